@@ -1,0 +1,211 @@
+"""Pure-Python restatement of the work-item planner in libpsa.so (psa_plan).
+
+TEST INFRASTRUCTURE (see ``oracle/__init__.py``). The reference has no
+work-item table; its only index table is the implicit stacked-row cursor of
+``attention.py:174`` / ``:182-200`` (request r owns rows
+[sum_{j<r} n_j, +n_r) of the group's stacked queries). The C++ planner
+generalises that cursor to (group, kv head, row range, KV chunk) work items
+and merge units; this module restates it line for line so that
+``tests/test_plan.py`` can require byte-identical int32 tables.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+
+ITEM_WORDS = 16
+UNIT_WORDS = 8
+(IT_KIND, IT_GROUP, IT_HEAD, IT_ROW0, IT_ROWS, IT_REQUEST, IT_PK0, IT_PK1, IT_DK0, IT_DK1,
+ IT_UNIT0, IT_UNIT1, IT_WSROW, IT_CANON) = range(14)
+(UN_GROUP, UN_HEAD, UN_ROW0, UN_ROWS, UN_CBEGIN, UN_CCOUNT) = range(6)
+KIND_VEC, KIND_TILE = 0, 1
+TILE_M = 128
+VEC_ROWS = 8
+CHUNK_ALIGN = 64
+BYTE_WEIGHT = 356
+VEC_FLOP_WEIGHT = 32
+RIDGE = 257
+DTYPE_BYTES = {0: 4, 1: 2, 2: 2, 3: 8}  # psa_dtype: F32, BF16, F16, F64
+
+
+def _cdiv(a, b):
+    return (a + b - 1) // b
+
+
+def _rup(a, b):
+    return _cdiv(a, b) * b
+
+
+def tiles_supported(dtype, d, dv, Hq, Hkv, disable_tiles=0):
+    if disable_tiles:
+        return False
+    if dtype not in (1, 2):
+        return False
+    if d not in (64, 128) or dv != d:
+        return False
+    return Hq // Hkv <= TILE_M
+
+
+def build_plan(G, R, Hq, Hkv, d, dv, dtype, cu_req, cu_q, cu_prefix, cu_distinct,
+               num_sms=148, ctas_per_sm=2, tile_min_rows=32, disable_tiles=0,
+               min_chunk_keys=256, max_chunk_keys=16384, target_waves=4):
+    """Returns dict(items, units, contribs, workspace_rows, chunk_keys, num_tile_items)."""
+    cu_req = [int(x) for x in cu_req]
+    cu_q = [int(x) for x in cu_q]
+    cu_prefix = [int(x) for x in cu_prefix]
+    cu_distinct = [int(x) for x in cu_distinct]
+    gqa = Hq // Hkv
+    tiles = tiles_supported(dtype, d, dv, Hq, Hkv, disable_tiles)
+    tile_rows = gqa * (TILE_M // gqa) if tiles else 0
+    elt = DTYPE_BYTES[dtype]
+    width = d + dv
+
+    def kind_for(rows):
+        return KIND_TILE if (tiles and rows >= tile_min_rows) else KIND_VEC
+
+    def step_for(kind):
+        return tile_rows if kind == KIND_TILE else VEC_ROWS
+
+    total = 0
+    for g in range(G):
+        tok0 = cu_q[cu_req[g]]
+        Ng = gqa * (cu_q[cu_req[g + 1]] - tok0)
+        P = cu_prefix[g + 1] - cu_prefix[g]
+        if P > 0:
+            total += _cdiv(Ng, step_for(kind_for(Ng))) * P
+        for r in range(cu_req[g], cu_req[g + 1]):
+            D = cu_distinct[r + 1] - cu_distinct[r]
+            nr = gqa * (cu_q[r + 1] - cu_q[r])
+            if D > 0:
+                total += _cdiv(nr, step_for(kind_for(nr))) * D
+    total *= Hkv
+    target = max(1, num_sms) * max(1, ctas_per_sm) * max(1, target_waves)
+    chunk = _cdiv(total, target)
+    chunk = min(max(chunk, min_chunk_keys), max_chunk_keys)
+    chunk = _rup(max(chunk, 1), CHUNK_ALIGN)
+
+    def per(L):
+        n = _cdiv(L, chunk)
+        return _rup(_cdiv(L, n), CHUNK_ALIGN)
+
+    items, units, unit_items = [], [], []
+    for g in range(G):
+        tok0 = cu_q[cu_req[g]]
+        Ng = gqa * (cu_q[cu_req[g + 1]] - tok0)
+        P = cu_prefix[g + 1] - cu_prefix[g]
+        for h in range(Hkv):
+            first = len(items)
+
+            def push(kind, row0, rows, req, pk0, pk1, dk0, dk1):
+                it = [0] * ITEM_WORDS
+                it[IT_KIND], it[IT_GROUP], it[IT_HEAD] = kind, g, h
+                it[IT_ROW0], it[IT_ROWS], it[IT_REQUEST] = row0, rows, req
+                it[IT_PK0], it[IT_PK1], it[IT_DK0], it[IT_DK1] = pk0, pk1, dk0, dk1
+                it[IT_WSROW] = -1
+                it[IT_CANON] = len(items)
+                items.append(it)
+
+            if P > 0:
+                kind = kind_for(Ng)
+                step, pp = step_for(kind), per(P)
+                for rb in range(0, Ng, step):
+                    for k0 in range(0, P, pp):
+                        push(kind, rb, min(step, Ng - rb), -1, k0, min(P, k0 + pp), 0, 0)
+            for r in range(cu_req[g], cu_req[g + 1]):
+                D = cu_distinct[r + 1] - cu_distinct[r]
+                if D <= 0:
+                    continue
+                rb = gqa * (cu_q[r] - tok0)
+                nr = gqa * (cu_q[r + 1] - cu_q[r])
+                kind = kind_for(nr)
+                step, pp = step_for(kind), per(D)
+                for o in range(0, nr, step):
+                    for k0 in range(0, D, pp):
+                        push(kind, rb + o, min(step, nr - o), r, 0, 0, k0, min(D, k0 + pp))
+            cuts = {0, Ng}
+            for it in items[first:]:
+                cuts.add(it[IT_ROW0])
+                cuts.add(it[IT_ROW0] + it[IT_ROWS])
+            for r in range(cu_req[g], cu_req[g + 1]):
+                cuts.add(gqa * (cu_q[r] - tok0))
+            cuts = sorted(cuts)
+            ubase = len(units)
+            for u in range(len(cuts) - 1):
+                rec = [0] * UNIT_WORDS
+                rec[UN_GROUP], rec[UN_HEAD] = g, h
+                rec[UN_ROW0], rec[UN_ROWS] = cuts[u], cuts[u + 1] - cuts[u]
+                units.append(rec)
+                unit_items.append([])
+            index = {c: i for i, c in enumerate(cuts)}
+            for i in range(first, len(items)):
+                it = items[i]
+                u0 = index[it[IT_ROW0]]
+                u1 = index[it[IT_ROW0] + it[IT_ROWS]]
+                it[IT_UNIT0], it[IT_UNIT1] = ubase + u0, ubase + u1
+                for u in range(u0, u1):
+                    unit_items[ubase + u].append(i)
+            for u in range(ubase, len(units)):
+                if not unit_items[u]:
+                    raise AssertionError("merge unit without contributions")
+
+    ws = 0
+    for it in items:
+        direct = all(len(unit_items[u]) == 1 for u in range(it[IT_UNIT0], it[IT_UNIT1]))
+        if not direct:
+            it[IT_WSROW] = ws
+            ws += it[IT_ROWS]
+    contribs = []
+    for u, rec in enumerate(units):
+        rec[UN_CBEGIN] = len(contribs)
+        rec[UN_CCOUNT] = len(unit_items[u])
+        for i in unit_items[u]:
+            it = items[i]
+            contribs.append(-1 if it[IT_WSROW] < 0 else it[IT_WSROW] + (rec[UN_ROW0] - it[IT_ROW0]))
+
+    cost = []
+    for it in items:
+        keys = (it[IT_PK1] - it[IT_PK0]) + (it[IT_DK1] - it[IT_DK0])
+        nbytes = (keys + it[IT_ROWS]) * width * elt
+        if it[IT_KIND] == KIND_TILE:
+            cost.append(max(nbytes * BYTE_WEIGHT, 2 * TILE_M * keys * width))
+        else:
+            cost.append(max(nbytes * BYTE_WEIGHT,
+                            2 * _rup(it[IT_ROWS], 4) * keys * width * VEC_FLOP_WEIGHT))
+    order = sorted(range(len(items)), key=lambda i: -cost[i])
+    return dict(
+        items=np.array([items[i] for i in order], dtype=np.int32).reshape(-1, ITEM_WORDS),
+        units=np.array(units, dtype=np.int32).reshape(-1, UNIT_WORDS),
+        contribs=np.array(contribs, dtype=np.int32),
+        workspace_rows=ws, chunk_keys=chunk,
+        num_tile_items=sum(1 for it in items if it[IT_KIND] == KIND_TILE))
+
+
+def group_costs(G, Hq, Hkv, d, dv, dtype, cu_req, cu_q, cu_prefix, cu_distinct):
+    elt = DTYPE_BYTES[dtype]
+    width = d + dv
+    out = []
+    for g in range(G):
+        P = int(cu_prefix[g + 1] - cu_prefix[g])
+        keys, tokens, pairs = P, 0, 0
+        for r in range(int(cu_req[g]), int(cu_req[g + 1])):
+            n = int(cu_q[r + 1] - cu_q[r])
+            D = int(cu_distinct[r + 1] - cu_distinct[r])
+            keys += D
+            tokens += n
+            pairs += n * (P + D)
+        nbytes = Hkv * keys * width * elt + tokens * Hq * width * elt
+        flops = 2 * Hq * pairs * width
+        out.append(max(nbytes * RIDGE, flops))
+    return np.array(out, dtype=np.int64)
+
+
+def shard_groups(cost, world):
+    """Greedy LPT: largest cost first, to the least-loaded rank (lowest rank on ties)."""
+    order = sorted(range(len(cost)), key=lambda g: -int(cost[g]))
+    load = [0] * world
+    owner = np.zeros(len(cost), dtype=np.int32)
+    for g in order:
+        best = min(range(world), key=lambda w: (load[w], w))
+        owner[g] = best
+        load[best] += int(cost[g])
+    return owner

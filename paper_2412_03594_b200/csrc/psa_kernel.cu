@@ -1,0 +1,455 @@
+// psa_kernel.cu — persistent prefix-shared attention kernel for sm_100a.
+//
+// One launch per call covers every work item of the plan (psa_plan.cpp): the
+// CTAs of a grid sized to (SMs x CTAs/SM) pull items from a global atomic
+// cursor in LPT order. Each item evaluates rows of one (group, kv head)
+// against one KV range — the reference's partial_attention (attention.py:78-98)
+// — and either finalises its rows directly (sole contributor) or stores the
+// unnormalised partial (o, m, l) in the workspace; the last item to arrive at a
+// merge unit combines that unit's partials in fixed contribution order
+// (merge, attention.py:101-119) and finalises (attention.py:122-126). No CTA
+// ever waits on another, so the single launch cannot deadlock.
+//
+// Paths:
+//   VEC  — CUDA-core decode path (few rows per item): see vec_item_*.
+//   TILE — tcgen05/TMEM/TMA tiles for stacked-row tiles of bf16/f16 d=64/128.
+#include <cuda.h>
+#include <cuda_bf16.h>
+#include <cuda_fp16.h>
+#include <cuda_runtime.h>
+
+#include <cfloat>
+#include <cmath>
+#include <cstdint>
+
+#include "../../include/psa.h"
+#include "psa_kernel.h"
+#include "psa_plan.h"
+
+namespace psa {
+namespace {
+
+constexpr int kThreads = 256;
+constexpr int kWarps = kThreads / 32;
+constexpr int kMaxLanesElems = 8;  // generic path: d, dv <= 256
+
+template <typename T> struct AccOf { using type = float; };
+template <> struct AccOf<double> { using type = double; };
+
+__device__ __forceinline__ float ld_acc(const float* p) { return *p; }
+__device__ __forceinline__ float ld_acc(const __nv_bfloat16* p) { return __bfloat162float(*p); }
+__device__ __forceinline__ float ld_acc(const __half* p) { return __half2float(*p); }
+__device__ __forceinline__ double ld_acc(const double* p) { return *p; }
+
+template <typename T> __device__ __forceinline__ T from_acc(float x);
+template <> __device__ __forceinline__ float from_acc<float>(float x) { return x; }
+template <> __device__ __forceinline__ __nv_bfloat16 from_acc<__nv_bfloat16>(float x) { return __float2bfloat16_rn(x); }
+template <> __device__ __forceinline__ __half from_acc<__half>(float x) { return __float2half_rn(x); }
+template <typename T> __device__ __forceinline__ T from_acc(double x) { return T(x); }
+
+// Softmax domain: float paths work in base 2 on logits pre-multiplied by
+// log2(e) (one FFMA per exponent); the float64 path works in base e exactly
+// like the reference.
+template <typename A> struct Dom;
+template <> struct Dom<float> {
+  static __device__ __forceinline__ float ex(float x) { return exp2f(x); }
+  static __device__ __forceinline__ float lg(float x) { return log2f(x); }
+  static constexpr float kLogE = 1.4426950408889634f;  // logits -> domain
+  static constexpr float kToNat = 0.6931471805599453f; // domain -> natural
+};
+template <> struct Dom<double> {
+  static __device__ __forceinline__ double ex(double x) { return exp(x); }
+  static __device__ __forceinline__ double lg(double x) { return log(x); }
+  static constexpr double kLogE = 1.0;
+  static constexpr double kToNat = 1.0;
+};
+
+template <typename A> __device__ __forceinline__ A neg_inf();
+template <> __device__ __forceinline__ float neg_inf<float>() { return -INFINITY; }
+template <> __device__ __forceinline__ double neg_inf<double>() { return -HUGE_VAL; }
+
+template <typename A>
+__device__ __forceinline__ A warp_sum(A v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+struct ItemRec {
+  int32_t kind, g, h, row0, nrows, req, pk0, pk1, dk0, dk1, u0, u1, ws_row;
+};
+
+__device__ __forceinline__ ItemRec load_item(const int32_t* rec) {
+  ItemRec it;
+  it.kind = __ldg(rec + kItKind);
+  it.g = __ldg(rec + kItGroup);
+  it.h = __ldg(rec + kItHead);
+  it.row0 = __ldg(rec + kItRow0);
+  it.nrows = __ldg(rec + kItRows);
+  it.req = __ldg(rec + kItRequest);
+  it.pk0 = __ldg(rec + kItPk0);
+  it.pk1 = __ldg(rec + kItPk1);
+  it.dk0 = __ldg(rec + kItDk0);
+  it.dk1 = __ldg(rec + kItDk1);
+  it.u0 = __ldg(rec + kItUnit0);
+  it.u1 = __ldg(rec + kItUnit1);
+  it.ws_row = __ldg(rec + kItWsRow);
+  return it;
+}
+
+// Final output of one (row, column) of group g / kv head h: out = o / l, or the
+// unnormalised partial with PSA_FLAG_PARTIAL_OUT. Column 0 also writes LSE/m/l.
+template <typename T, typename A>
+__device__ __forceinline__ void write_final(const KParams& p, int g, int h, int row, int c, A M,
+                                            A L, A O) {
+  const int64_t tok = __ldg(p.group_tok0 + g) + row / p.gqa;
+  const int64_t idx = tok * p.Hq + (int64_t)h * p.gqa + row % p.gqa;
+  if (p.flags & PSA_FLAG_PARTIAL_OUT) {
+    static_cast<A*>(p.out)[idx * p.dv + c] = O;
+    if (c == 0) {
+      static_cast<A*>(p.m_out)[idx] = M * A(Dom<A>::kToNat);
+      static_cast<A*>(p.l_out)[idx] = L;
+    }
+    return;
+  }
+  static_cast<T*>(p.out)[idx * p.dv + c] = from_acc<T>(O / L);
+  if (c == 0) {
+    if (!(L > A(0))) atomicOr(&p.ctrl->error, 1);
+    if (p.lse) p.lse[idx] = float((M + Dom<A>::lg(L)) * A(Dom<A>::kToNat));
+  }
+}
+
+// Emits one combined (row, column) value of an item: to the workspace when the
+// item shares its merge units, else straight to the output.
+template <typename T, typename A>
+__device__ __forceinline__ void emit(const KParams& p, const ItemRec& it, int r, int c, A M, A L,
+                                     A O) {
+  if (it.ws_row >= 0) {
+    const int64_t wr = (int64_t)it.ws_row + r;
+    static_cast<A*>(p.ws_o)[wr * p.dv + c] = O;
+    if (c == 0) {
+      static_cast<A*>(p.ws_ml)[wr * 2 + 0] = M;
+      static_cast<A*>(p.ws_ml)[wr * 2 + 1] = L;
+    }
+  } else {
+    write_final<T, A>(p, it.g, it.h, it.row0 + r, c, M, L, O);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Generic CUDA-core path: any dtype, any d, dv <= 256. Warps stride over keys,
+// lanes stride over the head dim; every key is a full online-softmax update
+// (exactly partial_attention's math, one key at a time). Rows go in passes of
+// RP; the eight warps' states are merged through shared memory.
+// ---------------------------------------------------------------------------
+template <typename T, typename A, int RP>
+__device__ void vec_item_generic(const KParams& p, const ItemRec& it, uint8_t* smem) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int d = p.d, dv = p.dv;
+  const A sc = A(p.scale) * A(Dom<A>::kLogE);
+  const T* Q = static_cast<const T*>(p.q);
+  const T* KP = static_cast<const T*>(p.kp);
+  const T* VP = static_cast<const T*>(p.vp);
+  const T* KD = static_cast<const T*>(p.kd);
+  const T* VD = static_cast<const T*>(p.vd);
+  const int np = it.pk1 - it.pk0, nk = np + (it.dk1 - it.dk0);
+  const int64_t pbase = (np > 0) ? __ldg(p.group_pbase + it.g) + it.pk0 : 0;
+  const int64_t dbase = (it.req >= 0) ? __ldg(p.req_dbase + it.req) + it.dk0 : 0;
+  const int64_t kstride = (int64_t)p.Hkv * d, vstride = (int64_t)p.Hkv * dv;
+  const int64_t tok0 = __ldg(p.group_tok0 + it.g);
+  A* sm_o = reinterpret_cast<A*>(smem);        // [kWarps][RP][dv]
+  A* sm_ml = sm_o + kWarps * RP * dv;          // [kWarps][RP][2]
+
+  for (int pr = 0; pr < it.nrows; pr += RP) {
+    const int nr = min(RP, it.nrows - pr);
+    A q[RP][kMaxLanesElems], o[RP][kMaxLanesElems], m[RP], l[RP];
+#pragma unroll
+    for (int r = 0; r < RP; ++r) {
+      const int row = it.row0 + pr + r;
+      const int64_t tok = tok0 + row / p.gqa;
+      const T* qr = Q + (tok * p.Hq + (int64_t)it.h * p.gqa + row % p.gqa) * d;
+#pragma unroll
+      for (int e = 0; e < kMaxLanesElems; ++e) {
+        const int c = lane + 32 * e;
+        q[r][e] = (r < nr && c < d) ? ld_acc(qr + c) : A(0);
+        o[r][e] = A(0);
+      }
+      m[r] = neg_inf<A>();
+      l[r] = A(0);
+    }
+    for (int j = warp; j < nk; j += kWarps) {
+      const T* kr;
+      const T* vr;
+      if (j < np) {
+        kr = KP + (pbase + j) * kstride + (int64_t)it.h * d;
+        vr = VP + (pbase + j) * vstride + (int64_t)it.h * dv;
+      } else {
+        kr = KD + (dbase + j - np) * kstride + (int64_t)it.h * d;
+        vr = VD + (dbase + j - np) * vstride + (int64_t)it.h * dv;
+      }
+      A kk[kMaxLanesElems], vv[kMaxLanesElems];
+#pragma unroll
+      for (int e = 0; e < kMaxLanesElems; ++e) {
+        const int c = lane + 32 * e;
+        kk[e] = c < d ? ld_acc(kr + c) : A(0);
+        vv[e] = c < dv ? ld_acc(vr + c) : A(0);
+      }
+#pragma unroll
+      for (int r = 0; r < RP; ++r) {
+        A s = A(0);
+#pragma unroll
+        for (int e = 0; e < kMaxLanesElems; ++e) s += q[r][e] * kk[e];
+        s = warp_sum(s);
+        const A x = s * sc;
+        const A mn = max(m[r], x);
+        const A alpha = Dom<A>::ex(m[r] - mn);
+        const A pe = Dom<A>::ex(x - mn);
+        l[r] = l[r] * alpha + pe;
+#pragma unroll
+        for (int e = 0; e < kMaxLanesElems; ++e) o[r][e] = o[r][e] * alpha + pe * vv[e];
+        m[r] = mn;
+      }
+    }
+#pragma unroll
+    for (int r = 0; r < RP; ++r) {
+#pragma unroll
+      for (int e = 0; e < kMaxLanesElems; ++e) {
+        const int c = lane + 32 * e;
+        if (c < dv) sm_o[(warp * RP + r) * dv + c] = o[r][e];
+      }
+      if (lane == 0) {
+        sm_ml[(warp * RP + r) * 2 + 0] = m[r];
+        sm_ml[(warp * RP + r) * 2 + 1] = l[r];
+      }
+    }
+    __syncthreads();
+    for (int idx = threadIdx.x; idx < nr * dv; idx += kThreads) {
+      const int r = idx / dv, c = idx - r * dv;
+      A M = neg_inf<A>();
+#pragma unroll
+      for (int w = 0; w < kWarps; ++w) M = max(M, sm_ml[(w * RP + r) * 2]);
+      A L = A(0), O = A(0);
+#pragma unroll
+      for (int w = 0; w < kWarps; ++w) {
+        const A lw = sm_ml[(w * RP + r) * 2 + 1];
+        if (lw > A(0)) {
+          const A f = Dom<A>::ex(sm_ml[(w * RP + r) * 2] - M);
+          L += f * lw;
+          O += f * sm_o[(w * RP + r) * dv + c];
+        }
+      }
+      emit<T, A>(p, it, pr + r, c, M, L, O);
+    }
+    __syncthreads();
+  }
+}
+
+// Last arriver: combine the unit's partials in contribution order and finalise.
+template <typename T, typename A>
+__device__ void merge_unit(const KParams& p, int u) {
+  const int32_t* U = p.units + (int64_t)u * kUnitWords;
+  const int g = __ldg(U + kUnGroup), h = __ldg(U + kUnHead);
+  const int row0 = __ldg(U + kUnRow0), nrows = __ldg(U + kUnRows);
+  const int cb = __ldg(U + kUnContribBegin), cc = __ldg(U + kUnContribCount);
+  const int32_t* C = p.contribs + cb;
+  const A* WO = static_cast<const A*>(p.ws_o);
+  const A* WML = static_cast<const A*>(p.ws_ml);
+  const int dv = p.dv;
+  for (int idx = threadIdx.x; idx < nrows * dv; idx += kThreads) {
+    const int r = idx / dv, c = idx - r * dv;
+    A M = neg_inf<A>();
+    for (int i = 0; i < cc; ++i) M = max(M, __ldcg(WML + ((int64_t)__ldg(C + i) + r) * 2));
+    A L = A(0), O = A(0);
+    for (int i = 0; i < cc; ++i) {
+      const int64_t wr = (int64_t)__ldg(C + i) + r;
+      const A li = __ldcg(WML + wr * 2 + 1);
+      if (li > A(0)) {
+        const A f = Dom<A>::ex(__ldcg(WML + wr * 2) - M);
+        L += f * li;
+        O += f * __ldcg(WO + wr * dv + c);
+      }
+    }
+    write_final<T, A>(p, g, h, row0 + r, c, M, L, O);
+  }
+}
+
+template <typename T>
+__global__ void __launch_bounds__(kThreads, 2) psa_persistent(const __grid_constant__ KParams p) {
+  using A = typename AccOf<T>::type;
+  constexpr int RP = sizeof(A) == 8 ? 2 : 4;
+  extern __shared__ __align__(1024) uint8_t smem[];
+  __shared__ int s_item;
+  __shared__ int s_nmerge;
+  __shared__ int s_merge[kTileM + 8];
+
+  for (;;) {
+    if (threadIdx.x == 0) s_item = atomicAdd(&p.ctrl->next_item, 1);
+    __syncthreads();
+    const int idx = s_item;
+    if (idx >= p.num_items) break;
+    const ItemRec it = load_item(p.items + (int64_t)idx * kItemWords);
+    vec_item_generic<T, A, RP>(p, it, smem);
+    if (it.ws_row >= 0) {
+      __threadfence();
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        int n = 0;
+        for (int u = it.u0; u < it.u1; ++u) {
+          const int need = __ldg(p.units + (int64_t)u * kUnitWords + kUnContribCount);
+          const int old = atomicAdd(p.unit_cnt + u, 1);
+          if (old == need - 1) {
+            s_merge[n++] = u;
+            p.unit_cnt[u] = 0;  // every contribution has arrived: reset for the next launch
+          }
+        }
+        s_nmerge = n;
+        __threadfence();
+      }
+      __syncthreads();
+      for (int i = 0; i < s_nmerge; ++i) merge_unit<T, A>(p, s_merge[i]);
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    __threadfence();
+    if (atomicAdd(&p.ctrl->done, 1) == (int)gridDim.x - 1) {
+      p.ctrl->next_item = 0;
+      p.ctrl->done = 0;
+      __threadfence();
+    }
+  }
+}
+
+// ---- standalone building blocks (PartialResult API) -----------------------
+
+template <typename A>
+__global__ void merge_kernel(int64_t rows, int32_t dv, const A* oa, const A* ma, const A* la,
+                             const A* ob, const A* mb, const A* lb, A* o, A* m, A* l) {
+  // One block per row, threads over columns (blockDim >= dv).
+  for (int64_t r = blockIdx.x; r < rows; r += gridDim.x) {
+    const A a_m = ma[r], b_m = mb[r], a_l = la[r], b_l = lb[r];
+    const A mm = max(a_m, b_m);
+    // attention.py:109-114: rows with l == 0 contribute nothing (exp(-inf - -inf) is masked).
+    const A fa = a_l > A(0) ? A(exp(double(a_m - mm))) : A(0);
+    const A fb = b_l > A(0) ? A(exp(double(b_m - mm))) : A(0);
+    const int c = threadIdx.x;
+    if (c < dv) o[r * dv + c] = fa * oa[r * dv + c] + fb * ob[r * dv + c];
+    __syncthreads();  // m/l outputs may alias inputs: every thread has read them
+    if (c == 0) {
+      m[r] = mm;
+      l[r] = fa * a_l + fb * b_l;
+    }
+    __syncthreads();
+  }
+}
+
+template <typename A, typename T>
+__global__ void finalize_kernel(int64_t rows, int32_t dv, const A* o, const A* l, T* out,
+                                int32_t* bad) {
+  const int64_t n = rows * dv;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = i / dv;
+    const A lr = l[r];
+    out[i] = T(o[i] / lr);
+    if (i % dv == 0 && !(lr > A(0))) atomicAdd(bad, 1);
+  }
+}
+
+template <typename T>
+__global__ void nonfinite_kernel(const T* x, int64_t n, int32_t* count) {
+  int local = 0;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    local += !isfinite((double)ld_acc(x + i));
+  local = __reduce_add_sync(0xffffffffu, local);
+  if ((threadIdx.x & 31) == 0 && local) atomicAdd(count, local);
+}
+
+template <typename T>
+int launch_typed(const KParams& p, int32_t num_sms, int32_t ctas_per_sm, void* stream) {
+  using A = typename AccOf<T>::type;
+  constexpr int RP = sizeof(A) == 8 ? 2 : 4;
+  const size_t smem = size_t(kWarps) * RP * (p.dv + 2) * sizeof(A);
+  cudaError_t e = cudaFuncSetAttribute(psa_persistent<T>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+  if (e != cudaSuccess) return e;
+  const int grid = num_sms * ctas_per_sm;
+  psa_persistent<T><<<grid, kThreads, smem, static_cast<cudaStream_t>(stream)>>>(p);
+  return cudaGetLastError();
+}
+
+inline int grid_for(int64_t n) {
+  int64_t b = (n + 255) / 256;
+  return int(b < 1 ? 1 : (b > 4096 ? 4096 : b));
+}
+
+}  // namespace
+
+int launch_psa(const KParams& p, int32_t dtype, int32_t num_sms, int32_t ctas_per_sm,
+               bool use_tiles, void* stream) {
+  (void)use_tiles;
+  switch (dtype) {
+    case PSA_DTYPE_F32: return launch_typed<float>(p, num_sms, ctas_per_sm, stream);
+    case PSA_DTYPE_BF16: return launch_typed<__nv_bfloat16>(p, num_sms, ctas_per_sm, stream);
+    case PSA_DTYPE_F16: return launch_typed<__half>(p, num_sms, ctas_per_sm, stream);
+    case PSA_DTYPE_F64: return launch_typed<double>(p, num_sms, ctas_per_sm, stream);
+    default: return cudaErrorInvalidValue;
+  }
+}
+
+size_t kernel_smem_bytes(int32_t dtype, bool use_tiles) {
+  (void)use_tiles;
+  return dtype == PSA_DTYPE_F64 ? size_t(kWarps) * 2 * (256 + 2) * 8
+                                : size_t(kWarps) * 4 * (256 + 2) * 4;
+}
+
+int launch_merge(int64_t rows, int32_t dv, int32_t dtype, const void* oa, const void* ma,
+                 const void* la, const void* ob, const void* mb, const void* lb, void* o,
+                 void* m, void* l, void* stream) {
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  // One block per row keeps the alias-safe barrier inside a row.
+  if (dv > 1024) return cudaErrorInvalidValue;
+  const int threads = ((dv + 31) / 32) * 32;
+  const int grid = int(rows < 65535 ? rows : 65535);
+  if (rows == 0) return cudaSuccess;
+  if (dtype == PSA_DTYPE_F64)
+    merge_kernel<double><<<grid, threads, 0, s>>>(
+        rows, dv, (const double*)oa, (const double*)ma, (const double*)la, (const double*)ob,
+        (const double*)mb, (const double*)lb, (double*)o, (double*)m, (double*)l);
+  else
+    merge_kernel<float><<<grid, threads, 0, s>>>(
+        rows, dv, (const float*)oa, (const float*)ma, (const float*)la, (const float*)ob,
+        (const float*)mb, (const float*)lb, (float*)o, (float*)m, (float*)l);
+  return cudaGetLastError();
+}
+
+int launch_finalize(int64_t rows, int32_t dv, int32_t dtype, const void* o, const void* l,
+                    void* out, int32_t* bad, void* stream) {
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const int64_t n = rows * dv;
+  if (n == 0) return cudaSuccess;
+  if (dtype == PSA_DTYPE_F64)
+    finalize_kernel<double, double><<<grid_for(n), 256, 0, s>>>(rows, dv, (const double*)o,
+                                                              (const double*)l, (double*)out, bad);
+  else
+    finalize_kernel<float, float><<<grid_for(n), 256, 0, s>>>(rows, dv, (const float*)o,
+                                                            (const float*)l, (float*)out, bad);
+  return cudaGetLastError();
+}
+
+int launch_count_nonfinite(const void* data, int64_t n, int32_t dtype, int32_t* count,
+                           void* stream) {
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  if (n == 0) return cudaSuccess;
+  switch (dtype) {
+    case PSA_DTYPE_F32: nonfinite_kernel<<<grid_for(n), 256, 0, s>>>((const float*)data, n, count); break;
+    case PSA_DTYPE_BF16: nonfinite_kernel<<<grid_for(n), 256, 0, s>>>((const __nv_bfloat16*)data, n, count); break;
+    case PSA_DTYPE_F16: nonfinite_kernel<<<grid_for(n), 256, 0, s>>>((const __half*)data, n, count); break;
+    case PSA_DTYPE_F64: nonfinite_kernel<<<grid_for(n), 256, 0, s>>>((const double*)data, n, count); break;
+    default: return cudaErrorInvalidValue;
+  }
+  return cudaGetLastError();
+}
+
+}  // namespace psa

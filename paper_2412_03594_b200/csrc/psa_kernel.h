@@ -1,0 +1,58 @@
+// psa_kernel.h — host/device contract of the persistent prefix-shared attention kernel.
+#pragma once
+
+#include <cstddef>
+#include <cstdint>
+
+namespace psa {
+
+// Control block at the start of every workspace. Zero between launches: the
+// last CTA to leave resets next_item/done, the last arriver of a merge unit
+// resets that unit's counter, so consecutive launches need no memset.
+struct Ctrl {
+  int32_t next_item;  // global work queue cursor
+  int32_t done;       // CTAs that left the persistent loop
+  int32_t error;      // bit 0: a row was finalised with l <= 0
+  int32_t pad[13];
+};
+
+struct KParams {
+  const void* q;
+  const void* kp;
+  const void* vp;
+  const void* kd;
+  const void* vd;
+  void* out;
+  float* lse;
+  void* m_out;
+  void* l_out;
+  const int32_t* items;
+  const int32_t* units;
+  const int32_t* contribs;
+  const int64_t* group_tok0;   // [G] first token of each group
+  const int64_t* group_pbase;  // [G] cu_prefix[g]
+  const int64_t* req_dbase;    // [R] cu_distinct[r]
+  void* ws_o;                  // [ws_rows, dv] accumulate type
+  void* ws_ml;                 // [ws_rows, 2]  (m, l) accumulate type
+  int32_t* unit_cnt;           // [num_units]
+  Ctrl* ctrl;
+  int32_t num_items;
+  int32_t Hq, Hkv, gqa, d, dv;
+  uint32_t flags;
+  int32_t pad0;
+  double scale;
+};
+
+// Launches one persistent grid on `stream`. Returns a cudaError_t value.
+int launch_psa(const KParams& p, int32_t dtype, int32_t num_sms, int32_t ctas_per_sm,
+               bool use_tiles, void* stream);
+int launch_merge(int64_t rows, int32_t dv, int32_t dtype, const void* oa, const void* ma,
+                 const void* la, const void* ob, const void* mb, const void* lb, void* o,
+                 void* m, void* l, void* stream);
+int launch_finalize(int64_t rows, int32_t dv, int32_t dtype, const void* o, const void* l,
+                    void* out, int32_t* bad, void* stream);
+int launch_count_nonfinite(const void* data, int64_t n, int32_t dtype, int32_t* count,
+                           void* stream);
+size_t kernel_smem_bytes(int32_t dtype, bool use_tiles);
+
+}  // namespace psa
