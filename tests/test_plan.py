@@ -120,14 +120,13 @@ def test_plan_invariants_c3():
 
 @pytest.mark.parametrize("bad, msg", [
     (dict(cu_q=[0, 1, 1]), "positive dimensions"),
-    (dict(cu_prefix=[0, 0], cu_distinct=[0, 5, 5]), "neither prefix nor distinct"),
+    (dict(cu_prefix=[0, 0, 0], cu_distinct=[0, 5, 5]), "neither prefix nor distinct"),
     (dict(cu_req=[0, 2, 2]), "has no requests"),
+    (dict(cu_req=[0, 1, 3]), "end at num_requests"),
 ])
 def test_plan_rejects_invalid_offsets(bad, msg):
     off = dict(cu_req=[0, 1, 2], cu_q=[0, 1, 2], cu_prefix=[0, 4, 8], cu_distinct=[0, 5, 5])
     off.update(bad)
-    if len(off["cu_req"]) != len(off["cu_prefix"]):
-        off["cu_prefix"] = off["cu_prefix"][:len(off["cu_req"])]
     with pytest.raises(ValidationError, match=msg):
         P.plan_tables_host(off["cu_req"], off["cu_q"], off["cu_prefix"], off["cu_distinct"],
                            2, 1, 64, 64, torch.bfloat16, P.PlanOptions(num_sms=148))
