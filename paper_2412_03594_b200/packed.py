@@ -96,10 +96,12 @@ class PrefixSharedAttention:
         self.d = int(head_dim)
         self.dv = int(value_dim) if value_dim is not None else self.d
         self.dtype = dtype
-        self.device = torch.device(device) if device is not None else torch.device(
-            "cuda", torch.cuda.current_device())
-        if self.device.type != "cuda":
+        dev = torch.device(device) if device is not None else torch.device("cuda")
+        if dev.type != "cuda":
             raise ValidationError("the op runs on a CUDA device only (no CPU fallback)")
+        if dev.index is None:
+            dev = torch.device("cuda", torch.cuda.current_device())
+        self.device = dev
         self.scale = float(scale) if scale is not None else 1.0 / math.sqrt(self.d)
         self.options = options or PlanOptions()
         self.num_tokens = int(self.cu_q[-1])
