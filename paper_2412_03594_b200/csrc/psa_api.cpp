@@ -19,6 +19,7 @@ struct psa_plan {
   int32_t num_sms = 0, ctas_per_sm = 0;
   bool use_tiles = false;
   std::vector<int64_t> group_tok0, group_pbase, req_dbase;
+  int64_t num_tokens = 0, prefix_keys = 0, distinct_keys = 0;
   // workspace layout (byte offsets)
   size_t off_ctrl = 0, off_cnt = 0, off_items = 0, off_units = 0, off_contribs = 0;
   size_t off_tok0 = 0, off_pbase = 0, off_dbase = 0, off_wso = 0, off_wsml = 0, total = 0;
@@ -150,6 +151,9 @@ psa_status psa_plan_create(const psa_problem* prob, const psa_plan_opts* opts, p
     pl->group_pbase[g] = in.cu_prefix[g];
   }
   for (int32_t r = 0; r < in.R; ++r) pl->req_dbase[r] = in.cu_distinct[r];
+  pl->num_tokens = in.cu_q[in.R];
+  pl->prefix_keys = in.cu_prefix[in.G];
+  pl->distinct_keys = in.cu_distinct[in.R];
   pl->dims.cu_req = pl->dims.cu_q = pl->dims.cu_prefix = pl->dims.cu_distinct = nullptr;
   layout(pl);
   *out = pl;
@@ -235,6 +239,17 @@ psa_status psa_run(const psa_problem* prob, const psa_plan* pl, void* ws, size_t
   k.Hq = in.Hq; k.Hkv = in.Hkv; k.gqa = in.Hq / in.Hkv; k.d = in.d; k.dv = in.dv;
   k.flags = prob->flags;
   k.scale = prob->scale;
+  k.use_tiles = pl->use_tiles ? 1 : 0;
+  if (pl->use_tiles) {
+    const uintptr_t align = reinterpret_cast<uintptr_t>(prob->q) |
+                            reinterpret_cast<uintptr_t>(prob->k_prefix) |
+                            reinterpret_cast<uintptr_t>(prob->v_prefix) |
+                            reinterpret_cast<uintptr_t>(prob->k_distinct) |
+                            reinterpret_cast<uintptr_t>(prob->v_distinct);
+    if (align & 15) return fail(PSA_INVALID_ARGUMENT, "tensor-core path needs 16-byte aligned buffers");
+    int te = psa::encode_tile_maps(k, in.dtype, pl->num_tokens, pl->prefix_keys, pl->distinct_keys);
+    if (te != 0) return cuda_fail(te, "cuTensorMapEncodeTiled");
+  }
   int e = psa::launch_psa(k, in.dtype, pl->num_sms, pl->ctas_per_sm, pl->use_tiles, stream);
   if (e != 0) return cuda_fail(e, "psa kernel launch");
   return PSA_OK;

@@ -21,10 +21,12 @@
 #include <cfloat>
 #include <cmath>
 #include <cstdint>
+#include <cstring>
 
 #include "../../include/psa.h"
 #include "psa_kernel.h"
 #include "psa_plan.h"
+#include "psa_tile.cuh"
 
 namespace psa {
 namespace {
@@ -273,6 +275,10 @@ __device__ void merge_unit(const KParams& p, int u) {
   }
 }
 
+template <typename T> struct HasTiles { static constexpr bool v = false; };
+template <> struct HasTiles<__nv_bfloat16> { static constexpr bool v = true; };
+template <> struct HasTiles<__half> { static constexpr bool v = true; };
+
 template <typename T>
 __global__ void __launch_bounds__(kThreads, 2) psa_persistent(const __grid_constant__ KParams p) {
   using A = typename AccOf<T>::type;
@@ -281,6 +287,27 @@ __global__ void __launch_bounds__(kThreads, 2) psa_persistent(const __grid_const
   __shared__ int s_item;
   __shared__ int s_nmerge;
   __shared__ int s_merge[kTileM + 8];
+  __shared__ tile::Barriers s_bar;
+  __shared__ uint32_t s_tmem;
+
+  tile::State tst{0u, 0u, 0u};
+  const bool tiles = HasTiles<T>::v && p.use_tiles;
+  if (tiles) {
+    const int warp = threadIdx.x >> 5;
+    if (threadIdx.x == 0) tile::init_barriers(&s_bar);
+    if (warp == 4 && (threadIdx.x & 31) == 0) {
+      dev::tma_prefetch_desc(&p.tm_q);
+      dev::tma_prefetch_desc(&p.tm_kp);
+      dev::tma_prefetch_desc(&p.tm_vp);
+      dev::tma_prefetch_desc(&p.tm_kd);
+      dev::tma_prefetch_desc(&p.tm_vd);
+    }
+    if (warp == 5) dev::tmem_alloc<tile::kTmemCols>(&s_tmem);
+    dev::tc_fence_before();
+    __syncthreads();
+    dev::tc_fence_after();
+    tst.tmem = s_tmem;
+  }
 
   for (;;) {
     if (threadIdx.x == 0) s_item = atomicAdd(&p.ctrl->next_item, 1);
@@ -288,7 +315,15 @@ __global__ void __launch_bounds__(kThreads, 2) psa_persistent(const __grid_const
     const int idx = s_item;
     if (idx >= p.num_items) break;
     const ItemRec it = load_item(p.items + (int64_t)idx * kItemWords);
-    vec_item_generic<T, A, RP>(p, it, smem);
+    if constexpr (HasTiles<T>::v) {
+      if (it.kind == kItemTile) {
+        tile::tile_item<T>(p, it, smem, &s_bar, tst);
+      } else {
+        vec_item_generic<T, A, RP>(p, it, smem);
+      }
+    } else {
+      vec_item_generic<T, A, RP>(p, it, smem);
+    }
     if (it.ws_row >= 0) {
       __threadfence();
       __syncthreads();
@@ -308,7 +343,9 @@ __global__ void __launch_bounds__(kThreads, 2) psa_persistent(const __grid_const
       __syncthreads();
       for (int i = 0; i < s_nmerge; ++i) merge_unit<T, A>(p, s_merge[i]);
     }
+    if (tiles) dev::tc_fence_before();
     __syncthreads();
+    if (tiles) dev::tc_fence_after();
   }
   if (threadIdx.x == 0) {
     __threadfence();
@@ -317,6 +354,11 @@ __global__ void __launch_bounds__(kThreads, 2) psa_persistent(const __grid_const
       p.ctrl->done = 0;
       __threadfence();
     }
+  }
+  if (tiles) {
+    dev::tc_fence_before();
+    __syncthreads();
+    if ((threadIdx.x >> 5) == 5) dev::tmem_dealloc<tile::kTmemCols>(tst.tmem);
   }
 }
 
@@ -367,10 +409,20 @@ __global__ void nonfinite_kernel(const T* x, int64_t n, int32_t* count) {
 }
 
 template <typename T>
-int launch_typed(const KParams& p, int32_t num_sms, int32_t ctas_per_sm, void* stream) {
+size_t smem_for(const KParams& p) {
   using A = typename AccOf<T>::type;
   constexpr int RP = sizeof(A) == 8 ? 2 : 4;
-  const size_t smem = size_t(kWarps) * RP * (p.dv + 2) * sizeof(A);
+  size_t smem = size_t(kWarps) * RP * (p.dv + 2) * sizeof(A);
+  if (HasTiles<T>::v && p.use_tiles) {
+    const size_t t = tile::smem_bytes(p.d, p.dv);
+    if (t > smem) smem = t;
+  }
+  return smem;
+}
+
+template <typename T>
+int launch_typed(const KParams& p, int32_t num_sms, int32_t ctas_per_sm, void* stream) {
+  const size_t smem = smem_for<T>(p);
   cudaError_t e = cudaFuncSetAttribute(psa_persistent<T>,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
   if (e != cudaSuccess) return e;
@@ -402,6 +454,65 @@ size_t kernel_smem_bytes(int32_t dtype, bool use_tiles) {
   (void)use_tiles;
   return dtype == PSA_DTYPE_F64 ? size_t(kWarps) * 2 * (256 + 2) * 8
                                 : size_t(kWarps) * 4 * (256 + 2) * 4;
+}
+
+namespace {
+using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                              const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                              const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                              CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+EncodeFn encode_fn() {
+  static EncodeFn fn = [] {
+    void* f = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) !=
+            cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      f = nullptr;
+    return reinterpret_cast<EncodeFn>(f);
+  }();
+  return fn;
+}
+
+// rank-3 (d, Hkv, keys) map with a (64, 1, box_rows) box, 128-byte swizzle.
+int encode_kv(CUtensorMap* m, CUtensorMapDataType dt, const void* base, int64_t keys, int heads,
+              int dim, int box_rows) {
+  std::memset(m, 0, sizeof(*m));
+  if (keys <= 0 || base == nullptr) return 0;
+  cuuint64_t gdim[3] = {cuuint64_t(dim), cuuint64_t(heads), cuuint64_t(keys)};
+  cuuint64_t gstride[2] = {cuuint64_t(dim) * 2, cuuint64_t(dim) * heads * 2};
+  cuuint32_t box[3] = {64, 1, cuuint32_t(box_rows)};
+  cuuint32_t estr[3] = {1, 1, 1};
+  CUresult r = encode_fn()(m, dt, 3, const_cast<void*>(base), gdim, gstride, box, estr,
+                           CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                           CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS ? 0 : int(cudaErrorInvalidValue);
+}
+}  // namespace
+
+int encode_tile_maps(KParams& p, int32_t dtype, int64_t T, int64_t prefix_keys,
+                     int64_t distinct_keys) {
+  if (!encode_fn()) return int(cudaErrorNotSupported);
+  const CUtensorMapDataType dt = dtype == PSA_DTYPE_BF16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16
+                                                         : CU_TENSOR_MAP_DATA_TYPE_FLOAT16;
+  std::memset(&p.tm_q, 0, sizeof(p.tm_q));
+  {
+    const int gqa = p.gqa;
+    cuuint64_t gdim[4] = {cuuint64_t(p.d), cuuint64_t(gqa), cuuint64_t(p.Hkv), cuuint64_t(T)};
+    cuuint64_t gstride[3] = {cuuint64_t(p.d) * 2, cuuint64_t(p.d) * gqa * 2,
+                             cuuint64_t(p.d) * p.Hq * 2};
+    cuuint32_t box[4] = {64, cuuint32_t(gqa), 1, cuuint32_t(tile::kM / gqa)};
+    cuuint32_t estr[4] = {1, 1, 1, 1};
+    CUresult r = encode_fn()(&p.tm_q, dt, 4, const_cast<void*>(p.q), gdim, gstride, box, estr,
+                             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) return int(cudaErrorInvalidValue);
+  }
+  int e = encode_kv(&p.tm_kp, dt, p.kp, prefix_keys, p.Hkv, p.d, tile::kBN);
+  if (!e) e = encode_kv(&p.tm_vp, dt, p.vp, prefix_keys, p.Hkv, p.dv, tile::kBN);
+  if (!e) e = encode_kv(&p.tm_kd, dt, p.kd, distinct_keys, p.Hkv, p.d, tile::kBN);
+  if (!e) e = encode_kv(&p.tm_vd, dt, p.vd, distinct_keys, p.Hkv, p.dv, tile::kBN);
+  return e;
 }
 
 int launch_merge(int64_t rows, int32_t dv, int32_t dtype, const void* oa, const void* ma,

@@ -1,6 +1,8 @@
 // psa_kernel.h — host/device contract of the persistent prefix-shared attention kernel.
 #pragma once
 
+#include <cuda.h>
+
 #include <cstddef>
 #include <cstdint>
 
@@ -17,6 +19,12 @@ struct Ctrl {
 };
 
 struct KParams {
+  // TMA descriptors (TILE items only): q as 4-D (d, gqa, Hkv, T); k/v as 3-D (d, Hkv, keys).
+  alignas(64) CUtensorMap tm_q;
+  alignas(64) CUtensorMap tm_kp;
+  alignas(64) CUtensorMap tm_vp;
+  alignas(64) CUtensorMap tm_kd;
+  alignas(64) CUtensorMap tm_vd;
   const void* q;
   const void* kp;
   const void* vp;
@@ -39,9 +47,13 @@ struct KParams {
   int32_t num_items;
   int32_t Hq, Hkv, gqa, d, dv;
   uint32_t flags;
-  int32_t pad0;
+  int32_t use_tiles;  // the plan has TILE items: allocate TMEM, init barriers
   double scale;
 };
+
+// Encodes the five TMA descriptors of `p` (tokens T, prefix keys, distinct keys).
+int encode_tile_maps(KParams& p, int32_t dtype, int64_t T, int64_t prefix_keys,
+                     int64_t distinct_keys);
 
 // Launches one persistent grid on `stream`. Returns a cudaError_t value.
 int launch_psa(const KParams& p, int32_t dtype, int32_t num_sms, int32_t ctas_per_sm,

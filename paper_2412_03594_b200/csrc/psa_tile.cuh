@@ -1,0 +1,363 @@
+// psa_tile.cuh — TILE work items: a 128-row tile of stacked query rows of one
+// (group, kv head) against a KV range, on the 5th-gen tensor cores.
+//
+// This is the "matrix-vector -> matrix-matrix" transformation of the paper's
+// §2.2 (reference: the stacked prefix call, attention.py:174-179): all gqa
+// heads x tokens of a group's requests that share the prefix form the M=128
+// rows of one tcgen05 tile, so each prefix K/V byte fetched from HBM feeds
+// 128 rows.
+//
+// Per CTA (256 threads) the roles are:
+//   warps 0-3  softmax + epilogue: thread t owns row t == TMEM lane t
+//   warp 4     TMA producer (one lane): Q tile once, K/V blocks into a 2-stage ring
+//   warp 5     MMA issuer (one lane): S = Q K^T and O += P V with tcgen05.mma
+// TMEM (256 columns per CTA, 2 CTAs/SM): S at columns [0, 64), O at [128, 128+dv).
+// Shared memory (d = dv = 128): Q 32 KB, 2 x (K 16 KB + V 16 KB); the bf16 P
+// block of iteration j is written into K_j's stage once S_j = Q K_j^T is done.
+//
+// Online softmax (attention.py:95-98 per block, merge :101-119 across blocks)
+// runs in base 2 with a lazy rescale: O and l are rescaled only when a row's
+// max grows by more than 2^8, so the common case touches O in TMEM never.
+#pragma once
+
+#include "psa_device.cuh"
+
+namespace psa {
+namespace tile {
+
+constexpr int kBN = 64;          // keys per KV block (S tile N)
+constexpr int kM = 128;          // rows per tile (UMMA M)
+constexpr int kStages = 2;
+constexpr uint32_t kTmemCols = 256;
+constexpr uint32_t kTmemS = 0;
+constexpr uint32_t kTmemO = 128;
+constexpr float kRescaleThreshold = 8.0f;  // log2 units
+
+struct Barriers {
+  uint64_t q_full;
+  uint64_t k_full[kStages];
+  uint64_t v_full[kStages];
+  uint64_t kv_empty[kStages];
+  uint64_t s_full;
+  uint64_t s_free;
+  uint64_t p_full[kStages];  // per stage so a fast softmax can never lap the MMA waiter
+  uint64_t o_done;
+};
+
+// Running phase bookkeeping, identical in every thread of the CTA.
+struct State {
+  uint32_t blocks;  // KV blocks processed by this CTA's TILE items so far
+  uint32_t items;   // TILE items processed so far
+  uint32_t tmem;    // TMEM base address
+};
+
+__host__ __device__ constexpr size_t smem_bytes(int d, int dv) {
+  // Q + stages*(K+V) (+ separate P when it cannot alias a K stage) + 1 KB alignment slack
+  return size_t(kM) * d * 2 + size_t(kStages) * kBN * (d + dv) * 2 +
+         (d == 128 ? 0 : size_t(kM) * kBN * 2) + 1024;
+}
+
+__device__ __forceinline__ void init_barriers(Barriers* b) {
+  dev::mbar_init(&b->q_full, 1);
+  for (int s = 0; s < kStages; ++s) {
+    dev::mbar_init(&b->k_full[s], 1);
+    dev::mbar_init(&b->v_full[s], 1);
+    dev::mbar_init(&b->kv_empty[s], 1);
+  }
+  dev::mbar_init(&b->s_full, 1);
+  dev::mbar_init(&b->s_free, 4);
+  for (int s = 0; s < kStages; ++s) dev::mbar_init(&b->p_full[s], 4);
+  dev::mbar_init(&b->o_done, 1);
+  dev::fence_mbar_init();
+}
+
+struct Layout {
+  uint8_t* q;
+  uint8_t* k[kStages];
+  uint8_t* v[kStages];
+  uint8_t* p[kStages];
+};
+
+__device__ __forceinline__ Layout carve(uint8_t* smem_raw, int d, int dv) {
+  uint8_t* base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                             ~uintptr_t(1023));
+  Layout L;
+  L.q = base;
+  uint8_t* cur = base + kM * d * 2;
+  for (int s = 0; s < kStages; ++s) {
+    L.k[s] = cur;
+    cur += kBN * d * 2;
+    L.v[s] = cur;
+    cur += kBN * dv * 2;
+  }
+  for (int s = 0; s < kStages; ++s) L.p[s] = (d == 128) ? L.k[s] : cur;
+  return L;
+}
+
+// bf16/f16 pack of two floats
+template <typename T> __device__ __forceinline__ uint32_t pack2(float a, float b);
+template <> __device__ __forceinline__ uint32_t pack2<__nv_bfloat16>(float a, float b) {
+  __nv_bfloat162 h = __floats2bfloat162_rn(a, b);
+  return *reinterpret_cast<uint32_t*>(&h);
+}
+template <> __device__ __forceinline__ uint32_t pack2<__half>(float a, float b) {
+  __half2 h = __floats2half2_rn(a, b);
+  return *reinterpret_cast<uint32_t*>(&h);
+}
+template <typename T> struct AbFormat;
+template <> struct AbFormat<__nv_bfloat16> { static constexpr uint32_t v = 1; };
+template <> struct AbFormat<__half> { static constexpr uint32_t v = 0; };
+
+struct Block {
+  const CUtensorMap* km;
+  const CUtensorMap* vm;
+  int key;     // first key row in the K/V tensor
+  int nvalid;  // valid keys in this block (<= kBN)
+};
+
+template <typename ItemT>
+__device__ __forceinline__ Block block_at(const KParams& p, const ItemT& it, int jb, int nbA,
+                                          int64_t pbase, int64_t dbase) {
+  Block b;
+  if (jb < nbA) {
+    b.km = &p.tm_kp;
+    b.vm = &p.tm_vp;
+    b.key = int(pbase + it.pk0 + jb * kBN);
+    b.nvalid = min(kBN, it.pk1 - it.pk0 - jb * kBN);
+  } else {
+    const int j = jb - nbA;
+    b.km = &p.tm_kd;
+    b.vm = &p.tm_vd;
+    b.key = int(dbase + it.dk0 + j * kBN);
+    b.nvalid = min(kBN, it.dk1 - it.dk0 - j * kBN);
+  }
+  return b;
+}
+
+template <typename T, typename ItemT>
+__device__ void tile_item(const KParams& p, const ItemT& it, uint8_t* smem_raw, Barriers* bar,
+                          State& st) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int d = p.d, dv = p.dv;
+  const Layout L = carve(smem_raw, d, dv);
+  const int nbA = (it.pk1 - it.pk0 + kBN - 1) / kBN;
+  const int nbB = (it.dk1 - it.dk0 + kBN - 1) / kBN;
+  const int nb = nbA + nbB;
+  const int64_t pbase = nbA ? __ldg(p.group_pbase + it.g) : 0;
+  const int64_t dbase = (it.req >= 0) ? __ldg(p.req_dbase + it.req) : 0;
+  const uint32_t base_blk = st.blocks;
+  const int gqa = p.gqa;
+  const int tokens_per_tile = kM / gqa;
+  const uint32_t k_bytes = kBN * d * 2, v_bytes = kBN * dv * 2;
+
+  if (warp == 4) {
+    // ---------------- TMA producer ----------------
+    if (lane == 0) {
+      const int t_start = int(__ldg(p.group_tok0 + it.g) + it.row0 / gqa);
+      dev::mbar_arrive_expect_tx(&bar->q_full, uint32_t(tokens_per_tile * gqa) * d * 2);
+      for (int c = 0; c < d / 64; ++c)
+        dev::tma_load_4d(L.q + c * (kM * 128), &p.tm_q, &bar->q_full, c * 64, 0, it.h, t_start);
+      for (int jb = 0; jb < nb; ++jb) {
+        const uint32_t n = base_blk + jb, s = n & 1, ph = (n >> 1) & 1;
+        dev::mbar_wait(&bar->kv_empty[s], ph ^ 1);
+        const Block b = block_at(p, it, jb, nbA, pbase, dbase);
+        dev::mbar_arrive_expect_tx(&bar->k_full[s], k_bytes);
+        for (int c = 0; c < d / 64; ++c)
+          dev::tma_load_3d(L.k[s] + c * (kBN * 128), b.km, &bar->k_full[s], c * 64, it.h, b.key);
+        dev::mbar_arrive_expect_tx(&bar->v_full[s], v_bytes);
+        for (int c = 0; c < dv / 64; ++c)
+          dev::tma_load_3d(L.v[s] + c * (kBN * 128), b.vm, &bar->v_full[s], c * 64, it.h, b.key);
+      }
+    }
+  } else if (warp == 5) {
+    // ---------------- MMA issuer ----------------
+    if (lane == 0) {
+      constexpr uint32_t fmt = AbFormat<T>::v;
+      const uint32_t idesc_s = dev::umma_idesc_f16(fmt, kM, kBN, 0, 0);
+      const uint32_t idesc_o = dev::umma_idesc_f16(fmt, kM, uint32_t(dv), 0, 1);
+      const uint32_t tS = st.tmem + kTmemS, tO = st.tmem + kTmemO;
+      const uint32_t q_addr = dev::smem_u32(L.q);
+      dev::mbar_wait(&bar->q_full, st.items & 1);
+      dev::tc_fence_after();
+      auto issue_s = [&](int jb) {
+        const uint32_t n = base_blk + jb, s = n & 1;
+        dev::mbar_wait(&bar->k_full[s], (n >> 1) & 1);
+        dev::tc_fence_after();
+        const uint32_t k_addr = dev::smem_u32(L.k[s]);
+        for (int kk = 0; kk < d / 16; ++kk) {
+          const uint32_t c = kk >> 2, w = (kk & 3) * 32;
+          const uint64_t a = dev::umma_desc_sw128(q_addr + c * (kM * 128) + w, 16, 1024);
+          const uint64_t b = dev::umma_desc_sw128(k_addr + c * (kBN * 128) + w, 16, 1024);
+          dev::mma_f16_ss(tS, a, b, idesc_s, kk > 0);
+        }
+        dev::mma_commit(&bar->s_full);
+      };
+      issue_s(0);
+      for (int jb = 0; jb < nb; ++jb) {
+        const uint32_t n = base_blk + jb, s = n & 1;
+        if (jb + 1 < nb) {
+          dev::mbar_wait(&bar->s_free, n & 1);  // S_n is in registers: S TMEM reusable
+          dev::tc_fence_after();
+          issue_s(jb + 1);
+        }
+        dev::mbar_wait(&bar->p_full[s], (n >> 1) & 1);
+        dev::mbar_wait(&bar->v_full[s], (n >> 1) & 1);
+        dev::tc_fence_after();
+        const uint32_t p_addr = dev::smem_u32(L.p[s]);
+        const uint32_t v_addr = dev::smem_u32(L.v[s]);
+        for (int kk = 0; kk < kBN / 16; ++kk) {
+          const uint64_t a = dev::umma_desc_sw128(p_addr + kk * 32, 16, 1024);
+          const uint64_t b = dev::umma_desc_sw128(v_addr + kk * (16 * 128), kBN * 128, 1024);
+          dev::mma_f16_ss(tO, a, b, idesc_o, (jb > 0 || kk > 0));
+        }
+        dev::mma_commit(&bar->kv_empty[s]);
+        dev::mma_commit(&bar->o_done);
+      }
+    }
+  } else if (warp < 4) {
+    // ---------------- softmax + epilogue (row = threadIdx.x) ----------------
+    const int row = threadIdx.x;
+    const uint32_t lane_base = uint32_t(warp * 32) << 16;
+    const uint32_t tS = st.tmem + kTmemS + lane_base, tO = st.tmem + kTmemO + lane_base;
+    const float sc = float(p.scale) * 1.4426950408889634f;
+    float m = -INFINITY, l = 0.f;
+    for (int jb = 0; jb < nb; ++jb) {
+      const uint32_t n = base_blk + jb, s = n & 1;
+      const Block b = block_at(p, it, jb, nbA, pbase, dbase);
+      dev::mbar_wait(&bar->s_full, n & 1);
+      dev::tc_fence_after();
+      uint32_t r0[32], r1[32];
+      dev::tmem_ld32(tS, r0);
+      dev::tmem_ld32(tS + 32, r1);
+      dev::tmem_wait_ld();
+      dev::tc_fence_before();
+      __syncwarp();
+      if (lane == 0) dev::mbar_arrive(&bar->s_free);
+      float x[kBN];
+#pragma unroll
+      for (int i = 0; i < 32; ++i) {
+        x[i] = (i < b.nvalid) ? __uint_as_float(r0[i]) * sc : -INFINITY;
+        x[32 + i] = (32 + i < b.nvalid) ? __uint_as_float(r1[i]) * sc : -INFINITY;
+      }
+      float mb = x[0];
+#pragma unroll
+      for (int i = 1; i < kBN; ++i) mb = fmaxf(mb, x[i]);
+      float alpha = 1.f;
+      bool rescale = false;
+      if (m == -INFINITY) {
+        m = mb;
+      } else if (mb > m + kRescaleThreshold) {
+        alpha = exp2f(m - mb);
+        m = mb;
+        rescale = true;
+      }
+      if (__any_sync(0xffffffffu, rescale)) {
+        // O holds PV_0..PV_{n-1}: wait for the last one, then scale rows in place.
+        dev::mbar_wait(&bar->o_done, (n - 1) & 1);
+        dev::tc_fence_after();
+        for (int c = 0; c < dv; c += 32) {
+          uint32_t o[32];
+          dev::tmem_ld32(tO + c, o);
+          dev::tmem_wait_ld();
+#pragma unroll
+          for (int i = 0; i < 32; ++i) o[i] = __float_as_uint(__uint_as_float(o[i]) * alpha);
+          dev::tmem_st32(tO + c, o);
+        }
+        dev::tmem_wait_st();
+      }
+      l *= alpha;
+      if (d != 128 && jb > 0) {
+        // separate single P buffer: PV_{n-1} must have finished reading it
+        dev::mbar_wait(&bar->o_done, (n - 1) & 1);
+      }
+      // P row (bf16) into the K-major SW128 layout: 16-byte chunk c of row r at
+      // r*128 + ((c ^ (r & 7)) * 16).
+      uint8_t* prow = L.p[s] + row * 128;
+#pragma unroll
+      for (int c = 0; c < kBN / 8; ++c) {
+        float e[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          e[i] = exp2f(x[c * 8 + i] - m);
+          l += e[i];
+        }
+        uint4 v;
+        v.x = pack2<T>(e[0], e[1]);
+        v.y = pack2<T>(e[2], e[3]);
+        v.z = pack2<T>(e[4], e[5]);
+        v.w = pack2<T>(e[6], e[7]);
+        *reinterpret_cast<uint4*>(prow + ((c ^ (row & 7)) * 16)) = v;
+      }
+      dev::fence_proxy_async_smem();
+      dev::tc_fence_before();
+      __syncwarp();
+      if (lane == 0) dev::mbar_arrive(&bar->p_full[s]);
+    }
+    // ---------------- epilogue ----------------
+    dev::mbar_wait(&bar->o_done, (base_blk + nb - 1) & 1);
+    dev::tc_fence_after();
+    const bool valid = row < it.nrows;
+    if (it.ws_row >= 0) {
+      float* wo = static_cast<float*>(p.ws_o) + ((int64_t)it.ws_row + row) * dv;
+      for (int c = 0; c < dv; c += 32) {
+        uint32_t o[32];
+        dev::tmem_ld32(tO + c, o);
+        dev::tmem_wait_ld();
+        if (valid) {
+#pragma unroll
+          for (int i = 0; i < 32; i += 4)
+            *reinterpret_cast<float4*>(wo + c + i) =
+                make_float4(__uint_as_float(o[i]), __uint_as_float(o[i + 1]),
+                            __uint_as_float(o[i + 2]), __uint_as_float(o[i + 3]));
+        }
+      }
+      if (valid) {
+        float* ml = static_cast<float*>(p.ws_ml) + ((int64_t)it.ws_row + row) * 2;
+        ml[0] = m;
+        ml[1] = l;
+      }
+    } else {
+      const int grow = it.row0 + row;
+      const int64_t tok = __ldg(p.group_tok0 + it.g) + grow / gqa;
+      const int64_t idx = tok * p.Hq + (int64_t)it.h * gqa + grow % gqa;
+      const bool partial_out = p.flags & PSA_FLAG_PARTIAL_OUT;
+      const float inv = 1.f / l;
+      for (int c = 0; c < dv; c += 32) {
+        uint32_t o[32];
+        dev::tmem_ld32(tO + c, o);
+        dev::tmem_wait_ld();
+        if (!valid) continue;
+        if (partial_out) {
+          float* dst = static_cast<float*>(p.out) + idx * dv + c;
+#pragma unroll
+          for (int i = 0; i < 32; ++i) dst[i] = __uint_as_float(o[i]);
+        } else {
+          uint8_t* dst = reinterpret_cast<uint8_t*>(static_cast<T*>(p.out) + idx * dv + c);
+#pragma unroll
+          for (int i = 0; i < 32; i += 8) {
+            uint4 v;
+            v.x = pack2<T>(__uint_as_float(o[i]) * inv, __uint_as_float(o[i + 1]) * inv);
+            v.y = pack2<T>(__uint_as_float(o[i + 2]) * inv, __uint_as_float(o[i + 3]) * inv);
+            v.z = pack2<T>(__uint_as_float(o[i + 4]) * inv, __uint_as_float(o[i + 5]) * inv);
+            v.w = pack2<T>(__uint_as_float(o[i + 6]) * inv, __uint_as_float(o[i + 7]) * inv);
+            *reinterpret_cast<uint4*>(dst + i * 2) = v;
+          }
+        }
+      }
+      if (valid) {
+        if (partial_out) {
+          static_cast<float*>(p.m_out)[idx] = m * 0.6931471805599453f;
+          static_cast<float*>(p.l_out)[idx] = l;
+        } else {
+          if (!(l > 0.f)) atomicOr(&p.ctrl->error, 1);
+          if (p.lse) p.lse[idx] = (m + log2f(l)) * 0.6931471805599453f;
+        }
+      }
+    }
+  }
+  st.blocks += nb;
+  st.items += 1;
+}
+
+}  // namespace tile
+}  // namespace psa
