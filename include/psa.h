@@ -100,7 +100,7 @@ typedef struct psa_plan_opts {
   int32_t min_chunk_keys; /* 0 = default (256) */
   int32_t max_chunk_keys; /* 0 = default (16384) */
   int32_t target_waves;   /* 0 = default (4) */
-  int32_t reserved;
+  int32_t disable_vec_fast; /* 1 = CUDA-core items use the generic path (diagnostics) */
 } psa_plan_opts;
 
 /* Read-only view of a plan's int32 tables (bit-exact with oracle/plan.py). */

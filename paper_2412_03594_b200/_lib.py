@@ -38,7 +38,7 @@ class PlanOpts(C.Structure):
     _fields_ = [
         ("num_sms", C.c_int32), ("ctas_per_sm", C.c_int32), ("tile_min_rows", C.c_int32),
         ("disable_tiles", C.c_int32), ("min_chunk_keys", C.c_int32),
-        ("max_chunk_keys", C.c_int32), ("target_waves", C.c_int32), ("reserved", C.c_int32),
+        ("max_chunk_keys", C.c_int32), ("target_waves", C.c_int32), ("disable_vec_fast", C.c_int32),
     ]
 
 

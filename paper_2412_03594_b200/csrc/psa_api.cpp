@@ -18,6 +18,7 @@ struct psa_plan {
   psa::PlanInput dims;  // pointers inside are NOT kept valid
   int32_t num_sms = 0, ctas_per_sm = 0;
   bool use_tiles = false;
+  bool use_vec_fast = false;
   std::vector<int64_t> group_tok0, group_pbase, req_dbase;
   int64_t num_tokens = 0, prefix_keys = 0, distinct_keys = 0;
   // workspace layout (byte offsets)
@@ -142,6 +143,9 @@ psa_status psa_plan_create(const psa_problem* prob, const psa_plan_opts* opts, p
   pl->num_sms = o.num_sms;
   pl->ctas_per_sm = o.ctas_per_sm;
   pl->use_tiles = pl->plan.num_tile_items > 0;
+  pl->use_vec_fast = psa::vec_fast_supported(prob->dtype, prob->head_dim, prob->value_dim) &&
+                     pl->plan.num_items > pl->plan.num_tile_items &&
+                     !(opts && opts->disable_vec_fast == 1);
   const auto& in = pl->dims;
   pl->group_tok0.resize(in.G);
   pl->group_pbase.resize(in.G);
@@ -240,13 +244,14 @@ psa_status psa_run(const psa_problem* prob, const psa_plan* pl, void* ws, size_t
   k.flags = prob->flags;
   k.scale = prob->scale;
   k.use_tiles = pl->use_tiles ? 1 : 0;
-  if (pl->use_tiles) {
+  k.use_vec_fast = (pl->use_vec_fast && !(prob->flags & PSA_FLAG_PARTIAL_OUT)) ? 1 : 0;
+  if (k.use_tiles || k.use_vec_fast) {
     const uintptr_t align = reinterpret_cast<uintptr_t>(prob->q) |
                             reinterpret_cast<uintptr_t>(prob->k_prefix) |
                             reinterpret_cast<uintptr_t>(prob->v_prefix) |
                             reinterpret_cast<uintptr_t>(prob->k_distinct) |
                             reinterpret_cast<uintptr_t>(prob->v_distinct);
-    if (align & 15) return fail(PSA_INVALID_ARGUMENT, "tensor-core path needs 16-byte aligned buffers");
+    if (align & 15) return fail(PSA_INVALID_ARGUMENT, "TMA paths need 16-byte aligned buffers");
     int te = psa::encode_tile_maps(k, in.dtype, pl->num_tokens, pl->prefix_keys, pl->distinct_keys);
     if (te != 0) return cuda_fail(te, "cuTensorMapEncodeTiled");
   }

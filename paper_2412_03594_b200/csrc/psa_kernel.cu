@@ -27,6 +27,7 @@
 #include "psa_kernel.h"
 #include "psa_plan.h"
 #include "psa_tile.cuh"
+#include "psa_vec.cuh"
 
 namespace psa {
 namespace {
@@ -289,9 +290,22 @@ __global__ void __launch_bounds__(kThreads, 2) psa_persistent(const __grid_const
   __shared__ int s_merge[kTileM + 8];
   __shared__ tile::Barriers s_bar;
   __shared__ uint32_t s_tmem;
+  __shared__ vec::Shared s_vec;
 
   tile::State tst{0u, 0u, 0u};
+  uint32_t vcnt = 0;  // per-warp count of VEC blocks (ring phase bookkeeping)
   const bool tiles = HasTiles<T>::v && p.use_tiles;
+  const bool vfast = HasTiles<T>::v && p.use_vec_fast;
+  if (vfast) {
+    if (threadIdx.x == 0) vec::init_barriers(&s_vec);
+    if (threadIdx.x == 32) {
+      dev::tma_prefetch_desc(&p.tmv_kp);
+      dev::tma_prefetch_desc(&p.tmv_vp);
+      dev::tma_prefetch_desc(&p.tmv_kd);
+      dev::tma_prefetch_desc(&p.tmv_vd);
+    }
+    __syncthreads();
+  }
   if (tiles) {
     const int warp = threadIdx.x >> 5;
     if (threadIdx.x == 0) tile::init_barriers(&s_bar);
@@ -318,6 +332,10 @@ __global__ void __launch_bounds__(kThreads, 2) psa_persistent(const __grid_const
     if constexpr (HasTiles<T>::v) {
       if (it.kind == kItemTile) {
         tile::tile_item<T>(p, it, smem, &s_bar, tst);
+      } else if (vfast) {
+        auto em = [&](int r, int c, float M, float L, float O) { emit<T, float>(p, it, r, c, M, L, O); };
+        if (p.d == 128) vec::vec_item<T, 128>(p, it, smem, &s_vec, vcnt, em);
+        else vec::vec_item<T, 64>(p, it, smem, &s_vec, vcnt, em);
       } else {
         vec_item_generic<T, A, RP>(p, it, smem);
       }
@@ -417,6 +435,10 @@ size_t smem_for(const KParams& p) {
     const size_t t = tile::smem_bytes(p.d, p.dv);
     if (t > smem) smem = t;
   }
+  if (HasTiles<T>::v && p.use_vec_fast) {
+    const size_t v = vec::smem_bytes(p.d);
+    if (v > smem) smem = v;
+  }
   return smem;
 }
 
@@ -474,29 +496,35 @@ EncodeFn encode_fn() {
   return fn;
 }
 
-// rank-3 (d, Hkv, keys) map with a (64, 1, box_rows) box, 128-byte swizzle.
+// rank-3 (d, Hkv, keys) map with a (box_inner, 1, box_rows) box.
 int encode_kv(CUtensorMap* m, CUtensorMapDataType dt, const void* base, int64_t keys, int heads,
-              int dim, int box_rows) {
+              int dim, int box_inner, int box_rows, bool swizzle128) {
   std::memset(m, 0, sizeof(*m));
   if (keys <= 0 || base == nullptr) return 0;
   cuuint64_t gdim[3] = {cuuint64_t(dim), cuuint64_t(heads), cuuint64_t(keys)};
   cuuint64_t gstride[2] = {cuuint64_t(dim) * 2, cuuint64_t(dim) * heads * 2};
-  cuuint32_t box[3] = {64, 1, cuuint32_t(box_rows)};
+  cuuint32_t box[3] = {cuuint32_t(box_inner), 1, cuuint32_t(box_rows)};
   cuuint32_t estr[3] = {1, 1, 1};
   CUresult r = encode_fn()(m, dt, 3, const_cast<void*>(base), gdim, gstride, box, estr,
-                           CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                           CU_TENSOR_MAP_INTERLEAVE_NONE,
+                           swizzle128 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_NONE,
                            CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   return r == CUDA_SUCCESS ? 0 : int(cudaErrorInvalidValue);
 }
 }  // namespace
+
+bool vec_fast_supported(int32_t dtype, int32_t d, int32_t dv) {
+  return (dtype == PSA_DTYPE_BF16 || dtype == PSA_DTYPE_F16) && d == dv && (d == 64 || d == 128);
+}
 
 int encode_tile_maps(KParams& p, int32_t dtype, int64_t T, int64_t prefix_keys,
                      int64_t distinct_keys) {
   if (!encode_fn()) return int(cudaErrorNotSupported);
   const CUtensorMapDataType dt = dtype == PSA_DTYPE_BF16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16
                                                          : CU_TENSOR_MAP_DATA_TYPE_FLOAT16;
-  std::memset(&p.tm_q, 0, sizeof(p.tm_q));
-  {
+  int e = 0;
+  if (p.use_tiles) {
+    std::memset(&p.tm_q, 0, sizeof(p.tm_q));
     const int gqa = p.gqa;
     cuuint64_t gdim[4] = {cuuint64_t(p.d), cuuint64_t(gqa), cuuint64_t(p.Hkv), cuuint64_t(T)};
     cuuint64_t gstride[3] = {cuuint64_t(p.d) * 2, cuuint64_t(p.d) * gqa * 2,
@@ -507,11 +535,17 @@ int encode_tile_maps(KParams& p, int32_t dtype, int64_t T, int64_t prefix_keys,
                              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
                              CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r != CUDA_SUCCESS) return int(cudaErrorInvalidValue);
+    e = encode_kv(&p.tm_kp, dt, p.kp, prefix_keys, p.Hkv, p.d, 64, tile::kBN, true);
+    if (!e) e = encode_kv(&p.tm_vp, dt, p.vp, prefix_keys, p.Hkv, p.dv, 64, tile::kBN, true);
+    if (!e) e = encode_kv(&p.tm_kd, dt, p.kd, distinct_keys, p.Hkv, p.d, 64, tile::kBN, true);
+    if (!e) e = encode_kv(&p.tm_vd, dt, p.vd, distinct_keys, p.Hkv, p.dv, 64, tile::kBN, true);
   }
-  int e = encode_kv(&p.tm_kp, dt, p.kp, prefix_keys, p.Hkv, p.d, tile::kBN);
-  if (!e) e = encode_kv(&p.tm_vp, dt, p.vp, prefix_keys, p.Hkv, p.dv, tile::kBN);
-  if (!e) e = encode_kv(&p.tm_kd, dt, p.kd, distinct_keys, p.Hkv, p.d, tile::kBN);
-  if (!e) e = encode_kv(&p.tm_vd, dt, p.vd, distinct_keys, p.Hkv, p.dv, tile::kBN);
+  if (!e && p.use_vec_fast) {
+    e = encode_kv(&p.tmv_kp, dt, p.kp, prefix_keys, p.Hkv, p.d, p.d, vec::kKB, false);
+    if (!e) e = encode_kv(&p.tmv_vp, dt, p.vp, prefix_keys, p.Hkv, p.dv, p.dv, vec::kKB, false);
+    if (!e) e = encode_kv(&p.tmv_kd, dt, p.kd, distinct_keys, p.Hkv, p.d, p.d, vec::kKB, false);
+    if (!e) e = encode_kv(&p.tmv_vd, dt, p.vd, distinct_keys, p.Hkv, p.dv, p.dv, vec::kKB, false);
+  }
   return e;
 }
 

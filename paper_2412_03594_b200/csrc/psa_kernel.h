@@ -25,6 +25,11 @@ struct KParams {
   alignas(64) CUtensorMap tm_vp;
   alignas(64) CUtensorMap tm_kd;
   alignas(64) CUtensorMap tm_vd;
+  // VEC fast path: k/v as 3-D (d, Hkv, keys), (d, 1, 8) boxes, no swizzle.
+  alignas(64) CUtensorMap tmv_kp;
+  alignas(64) CUtensorMap tmv_vp;
+  alignas(64) CUtensorMap tmv_kd;
+  alignas(64) CUtensorMap tmv_vd;
   const void* q;
   const void* kp;
   const void* vp;
@@ -47,13 +52,18 @@ struct KParams {
   int32_t num_items;
   int32_t Hq, Hkv, gqa, d, dv;
   uint32_t flags;
-  int32_t use_tiles;  // the plan has TILE items: allocate TMEM, init barriers
+  int32_t use_tiles;     // the plan has TILE items: allocate TMEM, init barriers
+  int32_t use_vec_fast;  // bf16/f16, d == dv in {64, 128}: TMA-staged decode path
+  int32_t pad1;
   double scale;
 };
 
-// Encodes the five TMA descriptors of `p` (tokens T, prefix keys, distinct keys).
+// Encodes the TMA descriptors of `p` (tokens T, prefix keys, distinct keys):
+// the TILE maps when p.use_tiles, the VEC maps when p.use_vec_fast.
 int encode_tile_maps(KParams& p, int32_t dtype, int64_t T, int64_t prefix_keys,
                      int64_t distinct_keys);
+// True when the VEC fast path applies to this dtype / head shape.
+bool vec_fast_supported(int32_t dtype, int32_t d, int32_t dv);
 
 // Launches one persistent grid on `stream`. Returns a cudaError_t value.
 int launch_psa(const KParams& p, int32_t dtype, int32_t num_sms, int32_t ctas_per_sm,

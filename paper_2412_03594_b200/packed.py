@@ -66,10 +66,12 @@ class PlanOptions:
     min_chunk_keys: int = 0
     max_chunk_keys: int = 0
     target_waves: int = 0
+    disable_vec_fast: int = 0
 
     def to_c(self) -> L.PlanOpts:
         return L.PlanOpts(self.num_sms, self.ctas_per_sm, self.tile_min_rows, self.disable_tiles,
-                          self.min_chunk_keys, self.max_chunk_keys, self.target_waves, 0)
+                          self.min_chunk_keys, self.max_chunk_keys, self.target_waves,
+                          self.disable_vec_fast)
 
 
 class PrefixSharedAttention:
