@@ -122,6 +122,47 @@ __device__ __forceinline__ void write_final(const KParams& p, int g, int h, int 
   }
 }
 
+template <typename T> __device__ __forceinline__ void store4(T* dst, float4 v, float s);
+template <> __device__ __forceinline__ void store4<float>(float* dst, float4 v, float s) {
+  *reinterpret_cast<float4*>(dst) = make_float4(v.x * s, v.y * s, v.z * s, v.w * s);
+}
+template <> __device__ __forceinline__ void store4<__nv_bfloat16>(__nv_bfloat16* dst, float4 v,
+                                                                  float s) {
+  __nv_bfloat162 a = __floats2bfloat162_rn(v.x * s, v.y * s), b = __floats2bfloat162_rn(v.z * s, v.w * s);
+  uint2 w;
+  w.x = *reinterpret_cast<uint32_t*>(&a);
+  w.y = *reinterpret_cast<uint32_t*>(&b);
+  *reinterpret_cast<uint2*>(dst) = w;
+}
+template <> __device__ __forceinline__ void store4<__half>(__half* dst, float4 v, float s) {
+  __half2 a = __floats2half2_rn(v.x * s, v.y * s), b = __floats2half2_rn(v.z * s, v.w * s);
+  uint2 w;
+  w.x = *reinterpret_cast<uint32_t*>(&a);
+  w.y = *reinterpret_cast<uint32_t*>(&b);
+  *reinterpret_cast<uint2*>(dst) = w;
+}
+
+// Four consecutive columns (c % 4 == 0, dv % 4 == 0) of a final row, fp32 accumulate.
+template <typename T>
+__device__ __forceinline__ void write_final4(const KParams& p, int g, int h, int row, int c,
+                                             float M, float L, float4 O) {
+  const int64_t tok = __ldg(p.group_tok0 + g) + row / p.gqa;
+  const int64_t idx = tok * p.Hq + (int64_t)h * p.gqa + row % p.gqa;
+  if (p.flags & PSA_FLAG_PARTIAL_OUT) {
+    store4<float>(static_cast<float*>(p.out) + idx * p.dv + c, O, 1.f);
+    if (c == 0) {
+      static_cast<float*>(p.m_out)[idx] = M * Dom<float>::kToNat;
+      static_cast<float*>(p.l_out)[idx] = L;
+    }
+    return;
+  }
+  store4<T>(static_cast<T*>(p.out) + idx * p.dv + c, O, 1.f / L);
+  if (c == 0) {
+    if (!(L > 0.f)) atomicOr(&p.ctrl->error, 1);
+    if (p.lse) p.lse[idx] = (M + log2f(L)) * Dom<float>::kToNat;
+  }
+}
+
 // Emits one combined (row, column) value of an item: to the workspace when the
 // item shares its merge units, else straight to the output.
 template <typename T, typename A>
@@ -139,6 +180,68 @@ __device__ __forceinline__ void emit(const KParams& p, const ItemRec& it, int r,
   }
 }
 
+template <typename T>
+__device__ __forceinline__ void emit4(const KParams& p, const ItemRec& it, int r, int c, float M,
+                                      float L, float4 O) {
+  if (it.ws_row >= 0) {
+    const int64_t wr = (int64_t)it.ws_row + r;
+    store4<float>(static_cast<float*>(p.ws_o) + wr * p.dv + c, O, 1.f);
+    if (c == 0) *reinterpret_cast<float2*>(static_cast<float*>(p.ws_ml) + wr * 2) = make_float2(M, L);
+  } else {
+    write_final4<T>(p, it.g, it.h, it.row0 + r, c, M, L, O);
+  }
+}
+
+// Combines the per-warp online-softmax states (m, l, o) of `nr` rows held in
+// shared memory — sm_o [kWarps][rp][dv], sm_ml [kWarps][rp][2] — and emits
+// every (row, column). Row statistics and the per-warp rescale factors are
+// computed once per row (s_f [kWarps][rp], s_M / s_L [rp]).
+template <typename T, typename A, typename Emit1, typename Emit4>
+__device__ __forceinline__ void combine_warps(int nr, int rp, int dv, const A* sm_o, const A* sm_ml,
+                                              A* s_f, A* s_M, A* s_L, Emit1&& e1, Emit4&& e4) {
+  if (threadIdx.x < nr) {
+    const int r = threadIdx.x;
+    A M = neg_inf<A>();
+#pragma unroll
+    for (int w = 0; w < kWarps; ++w) M = max(M, sm_ml[(w * rp + r) * 2]);
+    A L = A(0);
+#pragma unroll
+    for (int w = 0; w < kWarps; ++w) {
+      const A lw = sm_ml[(w * rp + r) * 2 + 1];
+      const A f = lw > A(0) ? Dom<A>::ex(sm_ml[(w * rp + r) * 2] - M) : A(0);
+      s_f[w * rp + r] = f;
+      L += f * lw;
+    }
+    s_M[r] = M;
+    s_L[r] = L;
+  }
+  __syncthreads();
+  if constexpr (sizeof(A) == 4) {
+    if ((dv & 3) == 0) {
+      const int q4 = dv >> 2;
+      for (int idx = threadIdx.x; idx < nr * q4; idx += kThreads) {
+        const int r = idx / q4, c = (idx - r * q4) * 4;
+        float4 O = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+        for (int w = 0; w < kWarps; ++w) {
+          const float f = s_f[w * rp + r];
+          const float4 v = *reinterpret_cast<const float4*>(sm_o + (w * rp + r) * dv + c);
+          O.x += f * v.x; O.y += f * v.y; O.z += f * v.z; O.w += f * v.w;
+        }
+        e4(r, c, s_M[r], s_L[r], O);
+      }
+      return;
+    }
+  }
+  for (int idx = threadIdx.x; idx < nr * dv; idx += kThreads) {
+    const int r = idx / dv, c = idx - r * dv;
+    A O = A(0);
+#pragma unroll
+    for (int w = 0; w < kWarps; ++w) O += s_f[w * rp + r] * sm_o[(w * rp + r) * dv + c];
+    e1(r, c, s_M[r], s_L[r], O);
+  }
+}
+
 // ---------------------------------------------------------------------------
 // Generic CUDA-core path: any dtype, any d, dv <= 256. Warps stride over keys,
 // lanes stride over the head dim; every key is a full online-softmax update
@@ -146,7 +249,8 @@ __device__ __forceinline__ void emit(const KParams& p, const ItemRec& it, int r,
 // RP; the eight warps' states are merged through shared memory.
 // ---------------------------------------------------------------------------
 template <typename T, typename A, int RP>
-__device__ void vec_item_generic(const KParams& p, const ItemRec& it, uint8_t* smem) {
+__device__ void vec_item_generic(const KParams& p, const ItemRec& it, uint8_t* smem, A* s_f,
+                                 A* s_M, A* s_L) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int d = p.d, dv = p.dv;
   const A sc = A(p.scale) * A(Dom<A>::kLogE);
@@ -226,30 +330,19 @@ __device__ void vec_item_generic(const KParams& p, const ItemRec& it, uint8_t* s
       }
     }
     __syncthreads();
-    for (int idx = threadIdx.x; idx < nr * dv; idx += kThreads) {
-      const int r = idx / dv, c = idx - r * dv;
-      A M = neg_inf<A>();
-#pragma unroll
-      for (int w = 0; w < kWarps; ++w) M = max(M, sm_ml[(w * RP + r) * 2]);
-      A L = A(0), O = A(0);
-#pragma unroll
-      for (int w = 0; w < kWarps; ++w) {
-        const A lw = sm_ml[(w * RP + r) * 2 + 1];
-        if (lw > A(0)) {
-          const A f = Dom<A>::ex(sm_ml[(w * RP + r) * 2] - M);
-          L += f * lw;
-          O += f * sm_o[(w * RP + r) * dv + c];
-        }
-      }
-      emit<T, A>(p, it, pr + r, c, M, L, O);
-    }
+    combine_warps<T, A>(
+        nr, RP, dv, sm_o, sm_ml, s_f, s_M, s_L,
+        [&](int r, int c, A M, A L, A O) { emit<T, A>(p, it, pr + r, c, M, L, O); },
+        [&](int r, int c, float M, float L, float4 O) { emit4<T>(p, it, pr + r, c, M, L, O); });
     __syncthreads();
   }
 }
 
 // Last arriver: combine the unit's partials in contribution order and finalise.
+// Phase 1 (thread per row): running max M and sum L over the contributions.
+// Phase 2 (thread per 4 columns): O = sum_i 2^(m_i - M) o_i.
 template <typename T, typename A>
-__device__ void merge_unit(const KParams& p, int u) {
+__device__ void merge_unit(const KParams& p, int u, A* s_M, A* s_L) {
   const int32_t* U = p.units + (int64_t)u * kUnitWords;
   const int g = __ldg(U + kUnGroup), h = __ldg(U + kUnHead);
   const int row0 = __ldg(U + kUnRow0), nrows = __ldg(U + kUnRows);
@@ -258,22 +351,55 @@ __device__ void merge_unit(const KParams& p, int u) {
   const A* WO = static_cast<const A*>(p.ws_o);
   const A* WML = static_cast<const A*>(p.ws_ml);
   const int dv = p.dv;
+  for (int r = threadIdx.x; r < nrows; r += kThreads) {
+    A M = neg_inf<A>(), L = A(0);
+    for (int i = 0; i < cc; ++i) {
+      const int64_t wr = (int64_t)__ldg(C + i) + r;
+      const A mi = __ldcg(WML + wr * 2), li = __ldcg(WML + wr * 2 + 1);
+      if (li > A(0)) {  // online combine in contribution order (attention.py:109-118)
+        const A mn = max(M, mi);
+        L = L * Dom<A>::ex(M - mn) + li * Dom<A>::ex(mi - mn);
+        M = mn;
+      }
+    }
+    s_M[r] = M;
+    s_L[r] = L;
+  }
+  __syncthreads();
+  if constexpr (sizeof(A) == 4) {
+    if ((dv & 3) == 0) {
+      const int q4 = dv >> 2;
+      for (int idx = threadIdx.x; idx < nrows * q4; idx += kThreads) {
+        const int r = idx / q4, c = (idx - r * q4) * 4;
+        const float M = s_M[r];
+        float4 O = make_float4(0.f, 0.f, 0.f, 0.f);
+        for (int i = 0; i < cc; ++i) {
+          const int64_t wr = (int64_t)__ldg(C + i) + r;
+          const float2 ml = __ldcg(reinterpret_cast<const float2*>(WML) + wr);
+          if (ml.y > 0.f) {
+            const float f = exp2f(ml.x - M);
+            const float4 v = __ldcg(reinterpret_cast<const float4*>(WO + wr * dv + c));
+            O.x += f * v.x; O.y += f * v.y; O.z += f * v.z; O.w += f * v.w;
+          }
+        }
+        write_final4<T>(p, g, h, row0 + r, c, M, s_L[r], O);
+      }
+      __syncthreads();
+      return;
+    }
+  }
   for (int idx = threadIdx.x; idx < nrows * dv; idx += kThreads) {
     const int r = idx / dv, c = idx - r * dv;
-    A M = neg_inf<A>();
-    for (int i = 0; i < cc; ++i) M = max(M, __ldcg(WML + ((int64_t)__ldg(C + i) + r) * 2));
-    A L = A(0), O = A(0);
+    const A M = s_M[r];
+    A O = A(0);
     for (int i = 0; i < cc; ++i) {
       const int64_t wr = (int64_t)__ldg(C + i) + r;
       const A li = __ldcg(WML + wr * 2 + 1);
-      if (li > A(0)) {
-        const A f = Dom<A>::ex(__ldcg(WML + wr * 2) - M);
-        L += f * li;
-        O += f * __ldcg(WO + wr * dv + c);
-      }
+      if (li > A(0)) O += Dom<A>::ex(__ldcg(WML + wr * 2) - M) * __ldcg(WO + wr * dv + c);
     }
-    write_final<T, A>(p, g, h, row0 + r, c, M, L, O);
+    write_final<T, A>(p, g, h, row0 + r, c, M, s_L[r], O);
   }
+  __syncthreads();
 }
 
 template <typename T> struct HasTiles { static constexpr bool v = false; };
@@ -291,6 +417,8 @@ __global__ void __launch_bounds__(kThreads, 2) psa_persistent(const __grid_const
   __shared__ tile::Barriers s_bar;
   __shared__ uint32_t s_tmem;
   __shared__ vec::Shared s_vec;
+  __shared__ A s_rowM[kTileM], s_rowL[kTileM];
+  __shared__ A s_fac[kWarps * 8];
 
   tile::State tst{0u, 0u, 0u};
   uint32_t vcnt = 0;  // per-warp count of VEC blocks (ring phase bookkeeping)
@@ -333,19 +461,21 @@ __global__ void __launch_bounds__(kThreads, 2) psa_persistent(const __grid_const
       if (it.kind == kItemTile) {
         tile::tile_item<T>(p, it, smem, &s_bar, tst);
       } else if (vfast) {
-        auto em = [&](int r, int c, float M, float L, float O) { emit<T, float>(p, it, r, c, M, L, O); };
-        if (p.d == 128) vec::vec_item<T, 128>(p, it, smem, &s_vec, vcnt, em);
-        else vec::vec_item<T, 64>(p, it, smem, &s_vec, vcnt, em);
+        auto e4 = [&](int pr_r, int c, float M, float L, float4 O) { emit4<T>(p, it, pr_r, c, M, L, O); };
+        if (p.d == 128) vec::vec_item<T, 128>(p, it, smem, &s_vec, vcnt, s_fac, s_rowM, s_rowL, e4);
+        else vec::vec_item<T, 64>(p, it, smem, &s_vec, vcnt, s_fac, s_rowM, s_rowL, e4);
       } else {
-        vec_item_generic<T, A, RP>(p, it, smem);
+        vec_item_generic<T, A, RP>(p, it, smem, s_fac, s_rowM, s_rowL);
       }
     } else {
-      vec_item_generic<T, A, RP>(p, it, smem);
+      vec_item_generic<T, A, RP>(p, it, smem, s_fac, s_rowM, s_rowL);
     }
     if (it.ws_row >= 0) {
-      __threadfence();
+      // Publish this item's partial rows: CTA barrier, then one gpu-scope fence by the
+      // thread that signals (release is cumulative over the barrier).
       __syncthreads();
       if (threadIdx.x == 0) {
+        __threadfence();
         int n = 0;
         for (int u = it.u0; u < it.u1; ++u) {
           const int need = __ldg(p.units + (int64_t)u * kUnitWords + kUnContribCount);
@@ -359,7 +489,7 @@ __global__ void __launch_bounds__(kThreads, 2) psa_persistent(const __grid_const
         __threadfence();
       }
       __syncthreads();
-      for (int i = 0; i < s_nmerge; ++i) merge_unit<T, A>(p, s_merge[i]);
+      for (int i = 0; i < s_nmerge; ++i) merge_unit<T, A>(p, s_merge[i], s_rowM, s_rowL);
     }
     if (tiles) dev::tc_fence_before();
     __syncthreads();

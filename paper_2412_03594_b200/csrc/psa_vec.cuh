@@ -62,9 +62,9 @@ template <> __device__ __forceinline__ float2 unpack2<__half>(uint32_t w) {
   return __half22float2(*reinterpret_cast<__half2*>(&w));
 }
 
-template <typename T, int D, typename ItemT, typename EmitFn>
+template <typename T, int D, typename ItemT, typename Emit4>
 __device__ void vec_item(const KParams& p, const ItemT& it, uint8_t* smem_raw, Shared* sh,
-                         uint32_t& cnt, EmitFn&& emit) {
+                         uint32_t& cnt, float* s_f, float* s_M, float* s_L, Emit4&& emit4) {
   using G = Geo<D>;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int kg = lane / G::LPK, ds = lane % G::LPK;
@@ -235,22 +235,34 @@ __device__ void vec_item(const KParams& p, const ItemT& it, uint8_t* smem_raw, S
       sm_ml[(warp * kRP + lane) * 2 + 1] = mine > 0 ? lp : 0.f;
     }
     __syncthreads();
-    for (int idx = threadIdx.x; idx < nr * D; idx += kWarps * 32) {
-      const int r = idx / D, cidx = idx - r * D;
+    // per-row statistics and per-warp factors once, then 4 columns per thread
+    if (threadIdx.x < nr) {
+      const int r = threadIdx.x;
       float M = -INFINITY;
 #pragma unroll
       for (int w = 0; w < kWarps; ++w) M = fmaxf(M, sm_ml[(w * kRP + r) * 2]);
-      float Lsum = 0.f, O = 0.f;
+      float Ls = 0.f;
 #pragma unroll
       for (int w = 0; w < kWarps; ++w) {
         const float lw = sm_ml[(w * kRP + r) * 2 + 1];
-        if (lw > 0.f) {
-          const float f = exp2f(sm_ml[(w * kRP + r) * 2] - M);
-          Lsum += f * lw;
-          O += f * sm_o[(w * kRP + r) * D + cidx];
-        }
+        const float f = lw > 0.f ? exp2f(sm_ml[(w * kRP + r) * 2] - M) : 0.f;
+        s_f[w * kRP + r] = f;
+        Ls += f * lw;
       }
-      emit(pr + r, cidx, M, Lsum, O);
+      s_M[r] = M;
+      s_L[r] = Ls;
+    }
+    __syncthreads();
+    for (int idx = threadIdx.x; idx < nr * (D / 4); idx += kWarps * 32) {
+      const int r = idx / (D / 4), c = (idx - r * (D / 4)) * 4;
+      float4 O = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+      for (int w = 0; w < kWarps; ++w) {
+        const float f = s_f[w * kRP + r];
+        const float4 v = *reinterpret_cast<const float4*>(sm_o + (w * kRP + r) * D + c);
+        O.x += f * v.x; O.y += f * v.y; O.z += f * v.z; O.w += f * v.w;
+      }
+      emit4(pr + r, c, s_M[r], s_L[r], O);
     }
     __syncthreads();
   }
