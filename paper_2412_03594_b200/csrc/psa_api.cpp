@@ -144,7 +144,6 @@ psa_status psa_plan_create(const psa_problem* prob, const psa_plan_opts* opts, p
   pl->ctas_per_sm = o.ctas_per_sm;
   pl->use_tiles = pl->plan.num_tile_items > 0;
   pl->use_vec_fast = psa::vec_fast_supported(prob->dtype, prob->head_dim, prob->value_dim) &&
-                     pl->plan.num_items > pl->plan.num_tile_items &&
                      !(opts && opts->disable_vec_fast == 1);
   const auto& in = pl->dims;
   pl->group_tok0.resize(in.G);

@@ -406,9 +406,15 @@ template <typename T> struct HasTiles { static constexpr bool v = false; };
 template <> struct HasTiles<__nv_bfloat16> { static constexpr bool v = true; };
 template <> struct HasTiles<__half> { static constexpr bool v = true; };
 
-template <typename T>
+// Kernel modes: which item paths are compiled in (keeps register allocation of
+// the hot paths free of the generic path's pressure).
+enum Mode : int { kModeGeneric = 0, kModeFast = 1, kModeTileGeneric = 2 };
+
+template <typename T, int kMode>
 __global__ void __launch_bounds__(kThreads, 2) psa_persistent(const __grid_constant__ KParams p) {
   using A = typename AccOf<T>::type;
+  constexpr bool kTiles = HasTiles<T>::v && kMode != kModeGeneric;
+  constexpr bool kVecFast = HasTiles<T>::v && kMode == kModeFast;
   constexpr int RP = sizeof(A) == 8 ? 2 : 4;
   extern __shared__ __align__(1024) uint8_t smem[];
   __shared__ int s_item;
@@ -422,8 +428,8 @@ __global__ void __launch_bounds__(kThreads, 2) psa_persistent(const __grid_const
 
   tile::State tst{0u, 0u, 0u};
   uint32_t vcnt = 0;  // per-warp count of VEC blocks (ring phase bookkeeping)
-  const bool tiles = HasTiles<T>::v && p.use_tiles;
-  const bool vfast = HasTiles<T>::v && p.use_vec_fast;
+  const bool tiles = kTiles && p.use_tiles;
+  const bool vfast = kVecFast;
   if (vfast) {
     if (threadIdx.x == 0) vec::init_barriers(&s_vec);
     if (threadIdx.x == 32) {
@@ -457,13 +463,13 @@ __global__ void __launch_bounds__(kThreads, 2) psa_persistent(const __grid_const
     const int idx = s_item;
     if (idx >= p.num_items) break;
     const ItemRec it = load_item(p.items + (int64_t)idx * kItemWords);
-    if constexpr (HasTiles<T>::v) {
+    if constexpr (kTiles) {
       if (it.kind == kItemTile) {
-        tile::tile_item<T>(p, it, smem, &s_bar, tst);
-      } else if (vfast) {
+        tst = tile::tile_item<T>(p, it, smem, &s_bar, tst);
+      } else if constexpr (kVecFast) {
         auto e4 = [&](int pr_r, int c, float M, float L, float4 O) { emit4<T>(p, it, pr_r, c, M, L, O); };
-        if (p.d == 128) vec::vec_item<T, 128>(p, it, smem, &s_vec, vcnt, s_fac, s_rowM, s_rowL, e4);
-        else vec::vec_item<T, 64>(p, it, smem, &s_vec, vcnt, s_fac, s_rowM, s_rowL, e4);
+        if (p.d == 128) vcnt = vec::vec_item<T, 128>(p, it, smem, &s_vec, vcnt, s_fac, s_rowM, s_rowL, e4);
+        else vcnt = vec::vec_item<T, 64>(p, it, smem, &s_vec, vcnt, s_fac, s_rowM, s_rowL, e4);
       } else {
         vec_item_generic<T, A, RP>(p, it, smem, s_fac, s_rowM, s_rowL);
       }
@@ -557,30 +563,39 @@ __global__ void nonfinite_kernel(const T* x, int64_t n, int32_t* count) {
 }
 
 template <typename T>
-size_t smem_for(const KParams& p) {
+size_t smem_for(const KParams& p, int mode) {
   using A = typename AccOf<T>::type;
   constexpr int RP = sizeof(A) == 8 ? 2 : 4;
-  size_t smem = size_t(kWarps) * RP * (p.dv + 2) * sizeof(A);
-  if (HasTiles<T>::v && p.use_tiles) {
+  size_t smem = mode == kModeFast ? 0 : size_t(kWarps) * RP * (p.dv + 2) * sizeof(A);
+  if (HasTiles<T>::v && mode != kModeGeneric && p.use_tiles) {
     const size_t t = tile::smem_bytes(p.d, p.dv);
     if (t > smem) smem = t;
   }
-  if (HasTiles<T>::v && p.use_vec_fast) {
+  if (HasTiles<T>::v && mode == kModeFast) {
     const size_t v = vec::smem_bytes(p.d);
     if (v > smem) smem = v;
   }
   return smem;
 }
 
-template <typename T>
-int launch_typed(const KParams& p, int32_t num_sms, int32_t ctas_per_sm, void* stream) {
-  const size_t smem = smem_for<T>(p);
-  cudaError_t e = cudaFuncSetAttribute(psa_persistent<T>,
+template <typename T, int kMode>
+int launch_mode(const KParams& p, int32_t num_sms, int32_t ctas_per_sm, void* stream) {
+  const size_t smem = smem_for<T>(p, kMode);
+  cudaError_t e = cudaFuncSetAttribute(psa_persistent<T, kMode>,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
   if (e != cudaSuccess) return e;
   const int grid = num_sms * ctas_per_sm;
-  psa_persistent<T><<<grid, kThreads, smem, static_cast<cudaStream_t>(stream)>>>(p);
+  psa_persistent<T, kMode><<<grid, kThreads, smem, static_cast<cudaStream_t>(stream)>>>(p);
   return cudaGetLastError();
+}
+
+template <typename T>
+int launch_typed(const KParams& p, int32_t num_sms, int32_t ctas_per_sm, void* stream) {
+  if constexpr (HasTiles<T>::v) {
+    if (p.use_vec_fast) return launch_mode<T, kModeFast>(p, num_sms, ctas_per_sm, stream);
+    if (p.use_tiles) return launch_mode<T, kModeTileGeneric>(p, num_sms, ctas_per_sm, stream);
+  }
+  return launch_mode<T, kModeGeneric>(p, num_sms, ctas_per_sm, stream);
 }
 
 inline int grid_for(int64_t n) {

@@ -71,26 +71,30 @@ __device__ __forceinline__ void init_barriers(Barriers* b) {
   dev::fence_mbar_init();
 }
 
+// Shared-memory layout, computed arithmetically (no runtime-indexed arrays:
+// those would live in local memory).
 struct Layout {
-  uint8_t* q;
-  uint8_t* k[kStages];
-  uint8_t* v[kStages];
-  uint8_t* p[kStages];
+  uint8_t* base;     // 1024-aligned
+  uint32_t q_bytes;  // kM * d * 2
+  uint32_t stage;    // K + V bytes of one stage
+  uint32_t k_bytes;  // kBN * d * 2
+  uint32_t p_off;    // offset of the separate P buffers (d != 128), else 0
+  __device__ __forceinline__ uint8_t* q() const { return base; }
+  __device__ __forceinline__ uint8_t* k(uint32_t s) const { return base + q_bytes + s * stage; }
+  __device__ __forceinline__ uint8_t* v(uint32_t s) const { return k(s) + k_bytes; }
+  __device__ __forceinline__ uint8_t* p(uint32_t s) const {
+    return p_off ? base + p_off : k(s);  // P_j aliases K_j's stage when the sizes agree
+  }
 };
 
 __device__ __forceinline__ Layout carve(uint8_t* smem_raw, int d, int dv) {
-  uint8_t* base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
-                                             ~uintptr_t(1023));
   Layout L;
-  L.q = base;
-  uint8_t* cur = base + kM * d * 2;
-  for (int s = 0; s < kStages; ++s) {
-    L.k[s] = cur;
-    cur += kBN * d * 2;
-    L.v[s] = cur;
-    cur += kBN * dv * 2;
-  }
-  for (int s = 0; s < kStages; ++s) L.p[s] = (d == 128) ? L.k[s] : cur;
+  L.base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                      ~uintptr_t(1023));
+  L.q_bytes = kM * d * 2;
+  L.k_bytes = kBN * d * 2;
+  L.stage = L.k_bytes + kBN * dv * 2;
+  L.p_off = (d == 128) ? 0u : L.q_bytes + kStages * L.stage;
   return L;
 }
 
@@ -135,8 +139,8 @@ __device__ __forceinline__ Block block_at(const KParams& p, const ItemT& it, int
 }
 
 template <typename T, typename ItemT>
-__device__ void tile_item(const KParams& p, const ItemT& it, uint8_t* smem_raw, Barriers* bar,
-                          State& st) {
+__device__ __forceinline__ State tile_item(const KParams& p, const ItemT& it, uint8_t* smem_raw,
+                                           Barriers* bar, State st) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int d = p.d, dv = p.dv;
   const Layout L = carve(smem_raw, d, dv);
@@ -156,17 +160,17 @@ __device__ void tile_item(const KParams& p, const ItemT& it, uint8_t* smem_raw, 
       const int t_start = int(__ldg(p.group_tok0 + it.g) + it.row0 / gqa);
       dev::mbar_arrive_expect_tx(&bar->q_full, uint32_t(tokens_per_tile * gqa) * d * 2);
       for (int c = 0; c < d / 64; ++c)
-        dev::tma_load_4d(L.q + c * (kM * 128), &p.tm_q, &bar->q_full, c * 64, 0, it.h, t_start);
+        dev::tma_load_4d(L.q() + c * (kM * 128), &p.tm_q, &bar->q_full, c * 64, 0, it.h, t_start);
       for (int jb = 0; jb < nb; ++jb) {
         const uint32_t n = base_blk + jb, s = n & 1, ph = (n >> 1) & 1;
         dev::mbar_wait(&bar->kv_empty[s], ph ^ 1);
         const Block b = block_at(p, it, jb, nbA, pbase, dbase);
         dev::mbar_arrive_expect_tx(&bar->k_full[s], k_bytes);
         for (int c = 0; c < d / 64; ++c)
-          dev::tma_load_3d(L.k[s] + c * (kBN * 128), b.km, &bar->k_full[s], c * 64, it.h, b.key);
+          dev::tma_load_3d(L.k(s) + c * (kBN * 128), b.km, &bar->k_full[s], c * 64, it.h, b.key);
         dev::mbar_arrive_expect_tx(&bar->v_full[s], v_bytes);
         for (int c = 0; c < dv / 64; ++c)
-          dev::tma_load_3d(L.v[s] + c * (kBN * 128), b.vm, &bar->v_full[s], c * 64, it.h, b.key);
+          dev::tma_load_3d(L.v(s) + c * (kBN * 128), b.vm, &bar->v_full[s], c * 64, it.h, b.key);
       }
     }
   } else if (warp == 5) {
@@ -176,14 +180,14 @@ __device__ void tile_item(const KParams& p, const ItemT& it, uint8_t* smem_raw, 
       const uint32_t idesc_s = dev::umma_idesc_f16(fmt, kM, kBN, 0, 0);
       const uint32_t idesc_o = dev::umma_idesc_f16(fmt, kM, uint32_t(dv), 0, 1);
       const uint32_t tS = st.tmem + kTmemS, tO = st.tmem + kTmemO;
-      const uint32_t q_addr = dev::smem_u32(L.q);
+      const uint32_t q_addr = dev::smem_u32(L.q());
       dev::mbar_wait(&bar->q_full, st.items & 1);
       dev::tc_fence_after();
       auto issue_s = [&](int jb) {
         const uint32_t n = base_blk + jb, s = n & 1;
         dev::mbar_wait(&bar->k_full[s], (n >> 1) & 1);
         dev::tc_fence_after();
-        const uint32_t k_addr = dev::smem_u32(L.k[s]);
+        const uint32_t k_addr = dev::smem_u32(L.k(s));
         for (int kk = 0; kk < d / 16; ++kk) {
           const uint32_t c = kk >> 2, w = (kk & 3) * 32;
           const uint64_t a = dev::umma_desc_sw128(q_addr + c * (kM * 128) + w, 16, 1024);
@@ -203,8 +207,8 @@ __device__ void tile_item(const KParams& p, const ItemT& it, uint8_t* smem_raw, 
         dev::mbar_wait(&bar->p_full[s], (n >> 1) & 1);
         dev::mbar_wait(&bar->v_full[s], (n >> 1) & 1);
         dev::tc_fence_after();
-        const uint32_t p_addr = dev::smem_u32(L.p[s]);
-        const uint32_t v_addr = dev::smem_u32(L.v[s]);
+        const uint32_t p_addr = dev::smem_u32(L.p(s));
+        const uint32_t v_addr = dev::smem_u32(L.v(s));
         for (int kk = 0; kk < kBN / 16; ++kk) {
           const uint64_t a = dev::umma_desc_sw128(p_addr + kk * 32, 16, 1024);
           const uint64_t b = dev::umma_desc_sw128(v_addr + kk * (16 * 128), kBN * 128, 1024);
@@ -233,15 +237,21 @@ __device__ void tile_item(const KParams& p, const ItemT& it, uint8_t* smem_raw, 
       dev::tc_fence_before();
       __syncwarp();
       if (lane == 0) dev::mbar_arrive(&bar->s_free);
-      float x[kBN];
+      // Raw S stays in r0/r1 (no second copy: keeps the softmax warps spill-free);
+      // masked keys become -inf in place. scale > 0, so max(s) * sc == max(s * sc).
+      if (b.nvalid < kBN) {
 #pragma unroll
-      for (int i = 0; i < 32; ++i) {
-        x[i] = (i < b.nvalid) ? __uint_as_float(r0[i]) * sc : -INFINITY;
-        x[32 + i] = (32 + i < b.nvalid) ? __uint_as_float(r1[i]) * sc : -INFINITY;
+        for (int i = 0; i < 32; ++i) {
+          if (i >= b.nvalid) r0[i] = 0xff800000u;
+          if (32 + i >= b.nvalid) r1[i] = 0xff800000u;
+        }
       }
-      float mb = x[0];
+      float mraw = __uint_as_float(r0[0]);
 #pragma unroll
-      for (int i = 1; i < kBN; ++i) mb = fmaxf(mb, x[i]);
+      for (int i = 1; i < 32; ++i) mraw = fmaxf(mraw, __uint_as_float(r0[i]));
+#pragma unroll
+      for (int i = 0; i < 32; ++i) mraw = fmaxf(mraw, __uint_as_float(r1[i]));
+      const float mb = mraw * sc;
       float alpha = 1.f;
       bool rescale = false;
       if (m == -INFINITY) {
@@ -251,8 +261,35 @@ __device__ void tile_item(const KParams& p, const ItemT& it, uint8_t* smem_raw, 
         m = mb;
         rescale = true;
       }
+      l *= alpha;
+      if (d != 128 && jb > 0) {
+        // separate single P buffer: PV_{n-1} must have finished reading it
+        dev::mbar_wait(&bar->o_done, (n - 1) & 1);
+      }
+      // P row (bf16) into the K-major SW128 layout: 16-byte chunk c of row r at
+      // r*128 + ((c ^ (r & 7)) * 16).
+      uint8_t* prow = L.p(s) + row * 128;
+      const float nm = -m;
+#pragma unroll
+      for (int c = 0; c < kBN / 8; ++c) {
+        float e[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          const int k = c * 8 + i;
+          const float raw = __uint_as_float(k < 32 ? r0[k] : r1[k - 32]);
+          e[i] = exp2f(fmaf(raw, sc, nm));
+          l += e[i];
+        }
+        uint4 v;
+        v.x = pack2<T>(e[0], e[1]);
+        v.y = pack2<T>(e[2], e[3]);
+        v.z = pack2<T>(e[4], e[5]);
+        v.w = pack2<T>(e[6], e[7]);
+        *reinterpret_cast<uint4*>(prow + ((c ^ (row & 7)) * 16)) = v;
+      }
       if (__any_sync(0xffffffffu, rescale)) {
-        // O holds PV_0..PV_{n-1}: wait for the last one, then scale rows in place.
+        // O holds PV_0..PV_{n-1}: wait for the last one, then scale rows in place
+        // (before signalling p_full, so PV_n accumulates onto the rescaled O).
         dev::mbar_wait(&bar->o_done, (n - 1) & 1);
         dev::tc_fence_after();
         for (int c = 0; c < dv; c += 32) {
@@ -264,29 +301,6 @@ __device__ void tile_item(const KParams& p, const ItemT& it, uint8_t* smem_raw, 
           dev::tmem_st32(tO + c, o);
         }
         dev::tmem_wait_st();
-      }
-      l *= alpha;
-      if (d != 128 && jb > 0) {
-        // separate single P buffer: PV_{n-1} must have finished reading it
-        dev::mbar_wait(&bar->o_done, (n - 1) & 1);
-      }
-      // P row (bf16) into the K-major SW128 layout: 16-byte chunk c of row r at
-      // r*128 + ((c ^ (r & 7)) * 16).
-      uint8_t* prow = L.p[s] + row * 128;
-#pragma unroll
-      for (int c = 0; c < kBN / 8; ++c) {
-        float e[8];
-#pragma unroll
-        for (int i = 0; i < 8; ++i) {
-          e[i] = exp2f(x[c * 8 + i] - m);
-          l += e[i];
-        }
-        uint4 v;
-        v.x = pack2<T>(e[0], e[1]);
-        v.y = pack2<T>(e[2], e[3]);
-        v.z = pack2<T>(e[4], e[5]);
-        v.w = pack2<T>(e[6], e[7]);
-        *reinterpret_cast<uint4*>(prow + ((c ^ (row & 7)) * 16)) = v;
       }
       dev::fence_proxy_async_smem();
       dev::tc_fence_before();
@@ -357,6 +371,7 @@ __device__ void tile_item(const KParams& p, const ItemT& it, uint8_t* smem_raw, 
   }
   st.blocks += nb;
   st.items += 1;
+  return st;
 }
 
 }  // namespace tile

@@ -62,9 +62,11 @@ template <> __device__ __forceinline__ float2 unpack2<__half>(uint32_t w) {
   return __half22float2(*reinterpret_cast<__half2*>(&w));
 }
 
+// Returns the warp's updated block count (ring phase bookkeeping).
 template <typename T, int D, typename ItemT, typename Emit4>
-__device__ void vec_item(const KParams& p, const ItemT& it, uint8_t* smem_raw, Shared* sh,
-                         uint32_t& cnt, float* s_f, float* s_M, float* s_L, Emit4&& emit4) {
+__device__ __forceinline__ uint32_t vec_item(const KParams& p, const ItemT& it, uint8_t* smem_raw,
+                                             Shared* sh, uint32_t cnt, float* s_f, float* s_M,
+                                             float* s_L, Emit4&& emit4) {
   using G = Geo<D>;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int kg = lane / G::LPK, ds = lane % G::LPK;
@@ -266,6 +268,7 @@ __device__ void vec_item(const KParams& p, const ItemT& it, uint8_t* smem_raw, S
     }
     __syncthreads();
   }
+  return cnt;
 }
 
 }  // namespace vec
