@@ -167,6 +167,11 @@ psa_status psa_finalize(int64_t rows, int32_t value_dim, int32_t dtype, const vo
 psa_status psa_count_nonfinite(const void* data, int64_t n, int32_t dtype, int32_t* count_dev,
                                void* stream);
 
+/* Diagnostics: subsequent psa_run calls on this host thread record, per work
+ * item, {cta | smid << 32, kind, t_start_ns, t_end_ns} (int64, %globaltimer)
+ * into the device buffer `buf` (capacity_items records). NULL/0 turns it off. */
+psa_status psa_debug_set_trace(void* buf, int64_t capacity_items);
+
 /* Group -> rank partition for multi-GPU sharding: greedy LPT
  * over per-group costs, deterministic ties (bit-exact with oracle/shard.py). */
 psa_status psa_shard_groups(int32_t num_groups, const int64_t* group_cost, int32_t world_size,

@@ -22,6 +22,7 @@ KIND_VEC, KIND_TILE = 0, 1
 TILE_M = 128
 VEC_ROWS = 8
 CHUNK_ALIGN = 64
+VEC_MAX_KEYS = 512
 BYTE_WEIGHT = 356
 VEC_FLOP_WEIGHT = 32
 RIDGE = 257
@@ -84,8 +85,9 @@ def build_plan(G, R, Hq, Hkv, d, dv, dtype, cu_req, cu_q, cu_prefix, cu_distinct
     chunk = min(max(chunk, min_chunk_keys), max_chunk_keys)
     chunk = _rup(max(chunk, 1), CHUNK_ALIGN)
 
-    def per(L):
-        n = _cdiv(L, chunk)
+    def per(L, kind):
+        ck = chunk if kind == KIND_TILE else min(chunk, VEC_MAX_KEYS)
+        n = _cdiv(L, ck)
         return _rup(_cdiv(L, n), CHUNK_ALIGN)
 
     items, units, unit_items = [], [], []
@@ -107,7 +109,7 @@ def build_plan(G, R, Hq, Hkv, d, dv, dtype, cu_req, cu_q, cu_prefix, cu_distinct
 
             if P > 0:
                 kind = kind_for(Ng)
-                step, pp = step_for(kind), per(P)
+                step, pp = step_for(kind), per(P, kind)
                 for rb in range(0, Ng, step):
                     for k0 in range(0, P, pp):
                         push(kind, rb, min(step, Ng - rb), -1, k0, min(P, k0 + pp), 0, 0)
@@ -118,7 +120,7 @@ def build_plan(G, R, Hq, Hkv, d, dv, dtype, cu_req, cu_q, cu_prefix, cu_distinct
                 rb = gqa * (cu_q[r] - tok0)
                 nr = gqa * (cu_q[r + 1] - cu_q[r])
                 kind = kind_for(nr)
-                step, pp = step_for(kind), per(D)
+                step, pp = step_for(kind), per(D, kind)
                 for o in range(0, nr, step):
                     for k0 in range(0, D, pp):
                         push(kind, rb + o, min(step, nr - o), r, 0, 0, k0, min(D, k0 + pp))
@@ -171,7 +173,8 @@ def build_plan(G, R, Hq, Hkv, d, dv, dtype, cu_req, cu_q, cu_prefix, cu_distinct
         else:
             cost.append(max(nbytes * BYTE_WEIGHT,
                             2 * _rup(it[IT_ROWS], 4) * keys * width * VEC_FLOP_WEIGHT))
-    order = sorted(range(len(items)), key=lambda i: -cost[i])
+    # TILE items first (CTA-level queue), then VEC items; each by cost descending
+    order = sorted(range(len(items)), key=lambda i: (items[i][IT_KIND] != KIND_TILE, -cost[i]))
     return dict(
         items=np.array([items[i] for i in order], dtype=np.int32).reshape(-1, ITEM_WORDS),
         units=np.array(units, dtype=np.int32).reshape(-1, UNIT_WORDS),

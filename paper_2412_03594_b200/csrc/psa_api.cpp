@@ -29,6 +29,8 @@ struct psa_plan {
 namespace {
 
 thread_local std::string g_error;
+thread_local int64_t* g_trace = nullptr;
+thread_local int64_t g_trace_cap = 0;
 
 psa_status fail(psa_status s, const std::string& msg) {
   g_error = msg;
@@ -239,9 +241,20 @@ psa_status psa_run(const psa_problem* prob, const psa_plan* pl, void* ws, size_t
   k.unit_cnt = reinterpret_cast<int32_t*>(base + pl->off_cnt);
   k.ctrl = reinterpret_cast<psa::Ctrl*>(base + pl->off_ctrl);
   k.num_items = pl->plan.num_items;
+  k.n_tile_items = pl->plan.num_tile_items;
+  {
+    // Every CTA starts on the tile queue: memory-bound tiles would otherwise be
+    // starved of memory-level parallelism by the deep per-warp VEC rings, and
+    // CTAs without a tile item move on to the VEC queue at once.
+    const int grid = pl->num_sms * pl->ctas_per_sm;
+    int nt = pl->plan.num_tile_items > 0 ? grid : 0;
+    k.n_tile_ctas = nt;
+  }
   k.Hq = in.Hq; k.Hkv = in.Hkv; k.gqa = in.Hq / in.Hkv; k.d = in.d; k.dv = in.dv;
   k.flags = prob->flags;
   k.scale = prob->scale;
+  k.trace = g_trace;
+  k.trace_cap = int32_t(g_trace_cap);
   k.use_tiles = pl->use_tiles ? 1 : 0;
   k.use_vec_fast = (pl->use_vec_fast && !(prob->flags & PSA_FLAG_PARTIAL_OUT)) ? 1 : 0;
   if (k.use_tiles || k.use_vec_fast) {
@@ -317,6 +330,14 @@ psa_status psa_count_nonfinite(const void* data, int64_t n, int32_t dtype, int32
   if (n < 0 || !count || (n > 0 && !data)) return fail(PSA_INVALID_ARGUMENT, "bad arguments");
   int e = psa::launch_count_nonfinite(data, n, dtype, count, stream);
   return e ? cuda_fail(e, "psa_count_nonfinite") : PSA_OK;
+}
+
+psa_status psa_debug_set_trace(void* buf, int64_t capacity_items) {
+  if (capacity_items < 0 || (capacity_items > 0 && !buf))
+    return fail(PSA_INVALID_ARGUMENT, "bad trace buffer");
+  g_trace = static_cast<int64_t*>(buf);
+  g_trace_cap = capacity_items > INT32_MAX ? INT32_MAX : capacity_items;
+  return PSA_OK;
 }
 
 psa_status psa_shard_groups(int32_t G, const int64_t* cost, int32_t world, int32_t* owner) {

@@ -78,6 +78,12 @@ __device__ __forceinline__ A warp_sum(A v) {
   return v;
 }
 
+__device__ __forceinline__ uint64_t globaltimer() {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
 struct ItemRec {
   int32_t kind, g, h, row0, nrows, req, pk0, pk1, dk0, dk1, u0, u1, ws_row;
 };
@@ -402,6 +408,52 @@ __device__ void merge_unit(const KParams& p, int u, A* s_M, A* s_L) {
   __syncthreads();
 }
 
+// Warp-per-row merge of one row of merge unit `u` (fp32 accumulate, dv % 4 == 0,
+// dv <= 128): every contribution's (m, l) and o are loaded in one round trip,
+// combined in contribution order and finalised (attention.py:101-126).
+template <typename T>
+__device__ __forceinline__ void merge_row_warp(const KParams& p, int u, int r) {
+  const int lane = threadIdx.x & 31;
+  const int32_t* U = p.units + (int64_t)u * kUnitWords;
+  const int g = __ldg(U + kUnGroup), h = __ldg(U + kUnHead), row0 = __ldg(U + kUnRow0);
+  const int cb = __ldg(U + kUnContribBegin), cc = __ldg(U + kUnContribCount);
+  const float* WO = static_cast<const float*>(p.ws_o);
+  const float2* WML = static_cast<const float2*>(p.ws_ml);
+  const int dv = p.dv, c = lane * 4;
+  float M = -INFINITY, L = 0.f;
+  float4 O = make_float4(0.f, 0.f, 0.f, 0.f);
+  for (int base = 0; base < cc; base += 32) {
+    const int n = min(32, cc - base);
+    int64_t wr = 0;
+    float2 ml = make_float2(-INFINITY, 0.f);
+    if (lane < n) {
+      wr = (int64_t)__ldg(p.contribs + cb + base + lane) + r;
+      ml = __ldcg(WML + wr);
+    }
+    float mc = ml.y > 0.f ? ml.x : -INFINITY;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) mc = fmaxf(mc, __shfl_xor_sync(0xffffffffu, mc, o));
+    const float mn = fmaxf(M, mc);
+    const float fo = M == -INFINITY ? 0.f : exp2f(M - mn);
+    float f = ml.y > 0.f ? exp2f(ml.x - mn) : 0.f;
+    float lsum = f * ml.y;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) lsum += __shfl_xor_sync(0xffffffffu, lsum, o);
+    L = L * fo + lsum;
+    O.x *= fo; O.y *= fo; O.z *= fo; O.w *= fo;
+    M = mn;
+    for (int i = 0; i < n; ++i) {
+      const float fi = __shfl_sync(0xffffffffu, f, i);
+      const int64_t wi = __shfl_sync(0xffffffffu, wr, i);
+      if (fi != 0.f && c < dv) {
+        const float4 v = __ldcg(reinterpret_cast<const float4*>(WO + wi * dv + c));
+        O.x += fi * v.x; O.y += fi * v.y; O.z += fi * v.z; O.w += fi * v.w;
+      }
+    }
+  }
+  if (c < dv) write_final4<T>(p, g, h, row0 + r, c, M, L, O);
+}
+
 template <typename T> struct HasTiles { static constexpr bool v = false; };
 template <> struct HasTiles<__nv_bfloat16> { static constexpr bool v = true; };
 template <> struct HasTiles<__half> { static constexpr bool v = true; };
@@ -409,6 +461,87 @@ template <> struct HasTiles<__half> { static constexpr bool v = true; };
 // Kernel modes: which item paths are compiled in (keeps register allocation of
 // the hot paths free of the generic path's pressure).
 enum Mode : int { kModeGeneric = 0, kModeFast = 1, kModeTileGeneric = 2 };
+
+__device__ __forceinline__ void trace_item(const KParams& p, int idx, int kind, int64_t t0) {
+  if (idx < p.trace_cap) {
+    uint32_t smid;
+    asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+    int64_t* t = p.trace + int64_t(idx) * 4;
+    t[0] = int64_t(blockIdx.x) | (int64_t(smid) << 32) | (int64_t(threadIdx.x >> 5) << 48);
+    t[1] = kind;
+    t[2] = t0;
+    t[3] = int64_t(globaltimer());
+  }
+}
+
+// CTA-level arrival at the merge units of item `it` (after its partial rows are
+// written): the last arriver of a unit merges that unit's rows, one warp per row.
+template <typename T, typename A>
+__device__ __forceinline__ void cta_arrive_and_merge(const KParams& p, const ItemRec& it,
+                                                     int* s_merge, int* s_nmerge, A* s_rowM,
+                                                     A* s_rowL) {
+  // Publish this item's partial rows: CTA barrier, then one gpu-scope fence by the
+  // thread that signals (release is cumulative over the barrier).
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    int n = 0;
+    for (int u = it.u0; u < it.u1; ++u) {
+      const int need = __ldg(p.units + (int64_t)u * kUnitWords + kUnContribCount);
+      const int old = atomicAdd(p.unit_cnt + u, 1);
+      if (old == need - 1) {
+        s_merge[n++] = u;
+        p.unit_cnt[u] = 0;  // every contribution has arrived: reset for the next launch
+      }
+    }
+    *s_nmerge = n;
+    if (n) __threadfence();  // acquire side for the partials about to be read
+  }
+  __syncthreads();
+  const int nm = *s_nmerge;
+  if (!nm) return;
+  if constexpr (sizeof(A) == 4) {
+    if ((p.dv & 3) == 0 && p.dv <= 128) {
+      const int warp = threadIdx.x >> 5;
+      int k = 0;
+      for (int i = 0; i < nm; ++i) {
+        const int u = s_merge[i];
+        const int rows = __ldg(p.units + (int64_t)u * kUnitWords + kUnRows);
+        for (int r = 0; r < rows; ++r, ++k)
+          if ((k & (kWarps - 1)) == warp) merge_row_warp<T>(p, u, r);
+      }
+      return;
+    }
+  }
+  for (int i = 0; i < nm; ++i) merge_unit<T, A>(p, s_merge[i], s_rowM, s_rowL);
+}
+
+// Warp-level arrival for a VEC item processed by one warp.
+template <typename T>
+__device__ __forceinline__ void warp_arrive_and_merge(const KParams& p, const ItemRec& it) {
+  const int lane = threadIdx.x & 31;
+  __threadfence();  // one warp-wide fence: publishes every lane's partial rows
+  __syncwarp();
+  uint32_t last = 0;
+  if (lane == 0) {
+    for (int u = it.u0; u < it.u1 && u - it.u0 < 32; ++u) {
+      const int need = __ldg(p.units + (int64_t)u * kUnitWords + kUnContribCount);
+      if (atomicAdd(p.unit_cnt + u, 1) == need - 1) {
+        last |= 1u << (u - it.u0);
+        p.unit_cnt[u] = 0;
+      }
+    }
+    if (last) __threadfence();
+  }
+  last = __shfl_sync(0xffffffffu, last, 0);
+  while (last) {
+    const int bit = __ffs(last) - 1;
+    last &= last - 1;
+    const int u = it.u0 + bit;
+    const int rows = __ldg(p.units + (int64_t)u * kUnitWords + kUnRows);
+    for (int r = 0; r < rows; ++r) merge_row_warp<T>(p, u, r);
+  }
+}
 
 template <typename T, int kMode>
 __global__ void __launch_bounds__(kThreads, 2) psa_persistent(const __grid_constant__ KParams p) {
@@ -426,11 +559,10 @@ __global__ void __launch_bounds__(kThreads, 2) psa_persistent(const __grid_const
   __shared__ A s_rowM[kTileM], s_rowL[kTileM];
   __shared__ A s_fac[kWarps * 8];
 
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   tile::State tst{0u, 0u, 0u};
-  uint32_t vcnt = 0;  // per-warp count of VEC blocks (ring phase bookkeeping)
   const bool tiles = kTiles && p.use_tiles;
-  const bool vfast = kVecFast;
-  if (vfast) {
+  if (kVecFast) {
     if (threadIdx.x == 0) vec::init_barriers(&s_vec);
     if (threadIdx.x == 32) {
       dev::tma_prefetch_desc(&p.tmv_kp);
@@ -441,9 +573,8 @@ __global__ void __launch_bounds__(kThreads, 2) psa_persistent(const __grid_const
     __syncthreads();
   }
   if (tiles) {
-    const int warp = threadIdx.x >> 5;
     if (threadIdx.x == 0) tile::init_barriers(&s_bar);
-    if (warp == 4 && (threadIdx.x & 31) == 0) {
+    if (warp == 4 && lane == 0) {
       dev::tma_prefetch_desc(&p.tm_q);
       dev::tma_prefetch_desc(&p.tm_kp);
       dev::tma_prefetch_desc(&p.tm_vp);
@@ -457,54 +588,75 @@ __global__ void __launch_bounds__(kThreads, 2) psa_persistent(const __grid_const
     tst.tmem = s_tmem;
   }
 
-  for (;;) {
-    if (threadIdx.x == 0) s_item = atomicAdd(&p.ctrl->next_item, 1);
-    __syncthreads();
-    const int idx = s_item;
-    if (idx >= p.num_items) break;
-    const ItemRec it = load_item(p.items + (int64_t)idx * kItemWords);
-    if constexpr (kTiles) {
-      if (it.kind == kItemTile) {
-        tst = tile::tile_item<T>(p, it, smem, &s_bar, tst);
-      } else if constexpr (kVecFast) {
-        auto e4 = [&](int pr_r, int c, float M, float L, float4 O) { emit4<T>(p, it, pr_r, c, M, L, O); };
-        if (p.d == 128) vcnt = vec::vec_item<T, 128>(p, it, smem, &s_vec, vcnt, s_fac, s_rowM, s_rowL, e4);
-        else vcnt = vec::vec_item<T, 64>(p, it, smem, &s_vec, vcnt, s_fac, s_rowM, s_rowL, e4);
+  // ---- CTA-level items from cursor `next_item`, indices [0, n) ------------------
+  auto cta_phase = [&](int n) {
+    if (tiles && threadIdx.x == 4 * 32) dev::fence_proxy_async_smem();
+    for (;;) {
+      if (threadIdx.x == 0) s_item = atomicAdd(&p.ctrl->next_item, 1);
+      __syncthreads();
+      const int idx = s_item;
+      if (idx >= n) break;
+      const ItemRec it = load_item(p.items + (int64_t)idx * kItemWords);
+      int64_t t0 = 0;
+      if (p.trace_cap > 0 && threadIdx.x == 0) t0 = int64_t(globaltimer());
+      if constexpr (kTiles) {
+        if (it.kind == kItemTile) tst = tile::tile_item<T>(p, it, smem, &s_bar, tst);
+        else if constexpr (!kVecFast) vec_item_generic<T, A, RP>(p, it, smem, s_fac, s_rowM, s_rowL);
       } else {
         vec_item_generic<T, A, RP>(p, it, smem, s_fac, s_rowM, s_rowL);
       }
-    } else {
-      vec_item_generic<T, A, RP>(p, it, smem, s_fac, s_rowM, s_rowL);
-    }
-    if (it.ws_row >= 0) {
-      // Publish this item's partial rows: CTA barrier, then one gpu-scope fence by the
-      // thread that signals (release is cumulative over the barrier).
+      if (it.ws_row >= 0) cta_arrive_and_merge<T, A>(p, it, s_merge, &s_nmerge, s_rowM, s_rowL);
+      if (p.trace_cap > 0 && threadIdx.x == 0) trace_item(p, idx, it.kind, t0);
+      if (tiles) dev::tc_fence_before();
       __syncthreads();
-      if (threadIdx.x == 0) {
-        __threadfence();
-        int n = 0;
-        for (int u = it.u0; u < it.u1; ++u) {
-          const int need = __ldg(p.units + (int64_t)u * kUnitWords + kUnContribCount);
-          const int old = atomicAdd(p.unit_cnt + u, 1);
-          if (old == need - 1) {
-            s_merge[n++] = u;
-            p.unit_cnt[u] = 0;  // every contribution has arrived: reset for the next launch
-          }
-        }
-        s_nmerge = n;
-        __threadfence();
+      if (tiles) dev::tc_fence_after();
+    }
+  };
+
+  if constexpr (kVecFast) {
+    // Two queues: TILE items [0, n_tile) are CTA-level, VEC items [n_tile, n) are
+    // warp-level. CTAs below n_tile_ctas start on the tile queue, the rest on the
+    // VEC queue; each drains the other queue once its own is empty.
+    auto warp_phase = [&]() {
+      uint8_t* ring = vec::warp_ring(smem, warp, p.d);
+      uint32_t vcnt = 0;  // ring phase bookkeeping (barriers are fresh every launch)
+      for (;;) {
+        int i = 0;
+        if (lane == 0) i = atomicAdd(&p.ctrl->next_vec, 1);
+        i = __shfl_sync(0xffffffffu, i, 0);
+        const int idx = p.n_tile_items + i;
+        if (idx >= p.num_items) break;
+        const ItemRec it = load_item(p.items + (int64_t)idx * kItemWords);
+        int64_t t0 = 0;
+        if (p.trace_cap > 0 && lane == 0) t0 = int64_t(globaltimer());
+        auto em = [&](int r, int c, float M, float L, const float (&o)[8]) {
+          emit4<T>(p, it, r, c, M, L, make_float4(o[0], o[1], o[2], o[3]));
+          emit4<T>(p, it, r, c + 4, M, L, make_float4(o[4], o[5], o[6], o[7]));
+        };
+        if (p.d == 128)
+          vcnt = vec::warp_item<T, 128>(p, it, ring, s_vec.full[warp], s_vec.p[warp], vcnt, em);
+        else
+          vcnt = vec::warp_item<T, 64>(p, it, ring, s_vec.full[warp], s_vec.p[warp], vcnt, em);
+        if (it.ws_row >= 0) warp_arrive_and_merge<T>(p, it);
+        if (p.trace_cap > 0 && lane == 0) trace_item(p, idx, it.kind, t0);
       }
+    };
+    if (int(blockIdx.x) < p.n_tile_ctas) {
+      cta_phase(p.n_tile_items);
+      warp_phase();
+    } else {
+      warp_phase();
       __syncthreads();
-      for (int i = 0; i < s_nmerge; ++i) merge_unit<T, A>(p, s_merge[i], s_rowM, s_rowL);
+      cta_phase(p.n_tile_items);
     }
-    if (tiles) dev::tc_fence_before();
-    __syncthreads();
-    if (tiles) dev::tc_fence_after();
+  } else {
+    cta_phase(p.num_items);
   }
   if (threadIdx.x == 0) {
     __threadfence();
     if (atomicAdd(&p.ctrl->done, 1) == (int)gridDim.x - 1) {
       p.ctrl->next_item = 0;
+      p.ctrl->next_vec = 0;
       p.ctrl->done = 0;
       __threadfence();
     }
@@ -512,7 +664,7 @@ __global__ void __launch_bounds__(kThreads, 2) psa_persistent(const __grid_const
   if (tiles) {
     dev::tc_fence_before();
     __syncthreads();
-    if ((threadIdx.x >> 5) == 5) dev::tmem_dealloc<tile::kTmemCols>(tst.tmem);
+    if (warp == 5) dev::tmem_dealloc<tile::kTmemCols>(tst.tmem);
   }
 }
 

@@ -15,7 +15,8 @@ struct Ctrl {
   int32_t next_item;  // global work queue cursor
   int32_t done;       // CTAs that left the persistent loop
   int32_t error;      // bit 0: a row was finalised with l <= 0
-  int32_t pad[13];
+  int32_t next_vec;   // warp-level VEC queue cursor (fast mode)
+  int32_t pad[12];
 };
 
 struct KParams {
@@ -50,12 +51,15 @@ struct KParams {
   int32_t* unit_cnt;           // [num_units]
   Ctrl* ctrl;
   int32_t num_items;
+  int32_t n_tile_items;  // items [0, n_tile_items) are TILE items (planner order)
+  int32_t n_tile_ctas;   // fast mode: CTAs that start on the tile queue
   int32_t Hq, Hkv, gqa, d, dv;
   uint32_t flags;
   int32_t use_tiles;     // the plan has TILE items: allocate TMEM, init barriers
   int32_t use_vec_fast;  // bf16/f16, d == dv in {64, 128}: TMA-staged decode path
-  int32_t pad1;
+  int32_t trace_cap;     // diagnostics: capacity (items) of `trace`, 0 = off
   double scale;
+  int64_t* trace;        // diagnostics: per item {cta | smid << 32, kind, t_start, t_end}
 };
 
 // Encodes the TMA descriptors of `p` (tokens T, prefix keys, distinct keys):

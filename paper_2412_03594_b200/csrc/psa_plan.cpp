@@ -111,6 +111,8 @@ std::string build_plan(const PlanInput& in, const PlanOptions& opt, Plan* out) {
   chunk = std::min<int64_t>(std::max<int64_t>(chunk, opt.min_chunk_keys), opt.max_chunk_keys);
   chunk = round_up(std::max<int64_t>(chunk, 1), kChunkAlign);
   const Chunking ck{chunk};
+  // One warp streams a VEC item: cap its keys so long segments spread over warps.
+  const Chunking ckv{std::min<int64_t>(chunk, kVecMaxKeys)};
   out->chunk_keys = int32_t(chunk);
 
   // 2. Canonical items and merge units.
@@ -139,7 +141,7 @@ std::string build_plan(const PlanInput& in, const PlanOptions& opt, Plan* out) {
       };
       if (P > 0) {
         const int32_t kind = kind_for(Ng);
-        const int64_t step = step_for(kind), per = ck.per(P);
+        const int64_t step = step_for(kind), per = (kind == kItemTile ? ck : ckv).per(P);
         for (int64_t rb = 0; rb < Ng; rb += step)
           for (int64_t k0 = 0; k0 < P; k0 += per)
             push(kind, rb, std::min(step, Ng - rb), -1, k0, std::min(P, k0 + per), 0, 0);
@@ -149,7 +151,7 @@ std::string build_plan(const PlanInput& in, const PlanOptions& opt, Plan* out) {
         if (D <= 0) continue;
         const int64_t rb = gqa * (in.cu_q[r] - tok0), nr = gqa * (in.cu_q[r + 1] - in.cu_q[r]);
         const int32_t kind = kind_for(nr);
-        const int64_t step = step_for(kind), per = ck.per(D);
+        const int64_t step = step_for(kind), per = (kind == kItemTile ? ck : ckv).per(D);
         for (int64_t o = 0; o < nr; o += step)
           for (int64_t k0 = 0; k0 < D; k0 += per)
             push(kind, rb + o, std::min(step, nr - o), r, 0, 0, k0, std::min(D, k0 + per));
@@ -215,10 +217,20 @@ std::string build_plan(const PlanInput& in, const PlanOptions& opt, Plan* out) {
       cost[i] = std::max(bytes * kByteWeight, 2 * round_up(it[kItRows], 4) * keys * width * kVecFlopWeight);
     }
   }
+  // Queue order: TILE items first (CTA-level queue), then VEC items (warp-level
+  // queue); each by cost descending, canonical index ascending.
   std::vector<int32_t> order(items.size());
   std::iota(order.begin(), order.end(), 0);
-  std::stable_sort(order.begin(), order.end(),
-                   [&](int32_t a, int32_t b) { return cost[a] > cost[b]; });
+  std::stable_sort(order.begin(), order.end(), [&](int32_t a, int32_t b) {
+    const bool ta = items[a][kItKind] == kItemTile, tb = items[b][kItKind] == kItemTile;
+    if (ta != tb) return ta;
+    return cost[a] > cost[b];
+  });
+  out->tile_cost = out->total_cost = 0;
+  for (size_t i = 0; i < items.size(); ++i) {
+    out->total_cost += cost[i];
+    if (items[i][kItKind] == kItemTile) out->tile_cost += cost[i];
+  }
 
   out->items.clear();
   out->items.reserve(items.size() * kItemWords);

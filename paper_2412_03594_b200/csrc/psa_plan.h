@@ -33,6 +33,7 @@ enum UnitField : int {
 constexpr int32_t kTileM = 128;        // tcgen05 M (rows per tile)
 constexpr int32_t kVecRows = 8;        // rows per CUDA-core item
 constexpr int32_t kChunkAlign = 64;    // KV chunk boundaries align to 64 keys
+constexpr int64_t kVecMaxKeys = 512;   // warp-level VEC items: at most 512 keys each
 constexpr int64_t kByteWeight = 356;   // ~ (tensor FLOP/clk/SM) / (HBM B/clk/SM)
 constexpr int64_t kVecFlopWeight = 32; // tensor / CUDA-core FLOP rate per SM
 constexpr int64_t kRidge = 257;        // measured B200 ridge (FLOP/B) for group costs
@@ -62,6 +63,7 @@ struct Plan {
   int32_t num_items = 0, num_units = 0, num_tile_items = 0;
   int64_t workspace_rows = 0;
   int32_t chunk_keys = 0;
+  int64_t tile_cost = 0, total_cost = 0;  // LPT cost model totals (host heuristics only)
 };
 
 // Returns "" on success, else the validation message (maps to PSA_INVALID_ARGUMENT).

@@ -6,17 +6,17 @@
 // partial_attention(q_r, dk_r, dv_r), attention.py:187-189). Every K/V byte is
 // read once per item and reused by all its rows.
 //
-// Data movement: each of the 8 warps owns a private 3-stage ring in shared
-// memory and streams 8-key blocks of K and V into it with TMA
-// (cp.async.bulk.tensor, one 2 KB box per operand), so each warp keeps up to
-// 12 KB in flight without any cross-warp synchronisation; lanes read the
-// staged rows with conflict-free 128-bit LDS.
-// Math: lane (key slot, 8-element d slice); QK^T partial dot products for
+// Granularity: ONE WARP per item. Each warp of the persistent CTA pulls VEC
+// items from its own queue cursor and owns a private 3-stage ring in shared
+// memory; it streams 8-key blocks of K and V into the ring with TMA
+// (cp.async.bulk.tensor, one 2 KB box per operand), so nothing synchronises
+// across warps and a warp's TMA stream stays busy for the whole item.
+// Math: lane = (key slot, 16-byte d slice); QK^T partial dot products for
 // (8 keys x 4 rows) are finished with a butterfly reduce-scatter (15 shuffles
-// for 16 sums, each lane ends with one full score), softmax statistics with 3
-// xor-shuffles per row, P goes through a 128-byte per-warp scratch, and PV
-// accumulates with packed fp32x2 FMAs (FFMA2). The eight warps' (m, l, o)
-// states are merged through shared memory at the end of the item.
+// for 16 sums, each lane ends with one full score), softmax statistics take 3
+// xor-shuffles per row, P goes through a 128-byte per-warp scratch and PV
+// accumulates with packed fp32x2 FMAs (FFMA2). The warp finishes its rows
+// itself: final output, or a partial for the in-kernel merge.
 #pragma once
 
 #include "psa_device.cuh"
@@ -24,7 +24,7 @@
 namespace psa {
 namespace vec {
 
-constexpr int kKB = 8;       // keys per warp block
+constexpr int kKB = 8;       // keys per block
 constexpr int kStages = 3;   // ring depth per warp
 constexpr int kRP = 4;       // rows per pass
 constexpr int kWarps = 8;
@@ -41,7 +41,9 @@ struct Geo {
   static_assert(J * 4 == LPK, "one finished score per lane");
 };
 
-__host__ __device__ constexpr size_t smem_bytes(int d) { return size_t(kWarps) * kStages * 2 * kKB * d * 2 + 128; }
+__host__ __device__ constexpr size_t smem_bytes(int d) {
+  return size_t(kWarps) * kStages * 2 * kKB * d * 2 + 128;
+}
 
 struct Shared {
   uint64_t full[kWarps][kStages];
@@ -54,6 +56,12 @@ __device__ __forceinline__ void init_barriers(Shared* s) {
   dev::fence_mbar_init();
 }
 
+__device__ __forceinline__ uint8_t* warp_ring(uint8_t* smem_raw, int warp, int d) {
+  uint8_t* ring = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 127) &
+                                             ~uintptr_t(127));
+  return ring + size_t(warp) * kStages * 2 * kKB * d * 2;
+}
+
 template <typename T> __device__ __forceinline__ float2 unpack2(uint32_t w);
 template <> __device__ __forceinline__ float2 unpack2<__nv_bfloat16>(uint32_t w) {
   return make_float2(__uint_as_float(w << 16), __uint_as_float(w & 0xffff0000u));
@@ -62,49 +70,42 @@ template <> __device__ __forceinline__ float2 unpack2<__half>(uint32_t w) {
   return __half22float2(*reinterpret_cast<__half2*>(&w));
 }
 
+// Processes VEC item `it` with the calling warp. `emit8(row_in_item, col, M, L, o[8])`
+// receives the 8 finished columns [col, col+8) of each row (M in log2 units).
 // Returns the warp's updated block count (ring phase bookkeeping).
-template <typename T, int D, typename ItemT, typename Emit4>
-__device__ __forceinline__ uint32_t vec_item(const KParams& p, const ItemT& it, uint8_t* smem_raw,
-                                             Shared* sh, uint32_t cnt, float* s_f, float* s_M,
-                                             float* s_L, Emit4&& emit4) {
+template <typename T, int D, typename ItemT, typename Emit8>
+__device__ __forceinline__ uint32_t warp_item(const KParams& p, const ItemT& it, uint8_t* ring,
+                                              uint64_t* full, float* pscratch, uint32_t cnt,
+                                              Emit8&& emit8) {
   using G = Geo<D>;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int lane = threadIdx.x & 31;
   const int kg = lane / G::LPK, ds = lane % G::LPK;
-  uint8_t* ring = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 127) &
-                                             ~uintptr_t(127));
-  uint8_t* my_ring = ring + warp * G::WARP;
   const int npA = it.pk1 - it.pk0, npB = it.dk1 - it.dk0;
   const int nbA = (npA + kKB - 1) / kKB, nb = nbA + (npB + kKB - 1) / kKB;
   const int64_t pbase = npA ? __ldg(p.group_pbase + it.g) + it.pk0 : 0;
   const int64_t dbase = (it.req >= 0) ? __ldg(p.req_dbase + it.req) + it.dk0 : 0;
-  const int mine = warp < nb ? (nb - warp + kWarps - 1) / kWarps : 0;
   const float sc = float(p.scale) * 1.4426950408889634f;
   const int64_t tok0 = __ldg(p.group_tok0 + it.g);
   const T* Q = static_cast<const T*>(p.q);
 
-  auto issue = [&](int i) {  // lane 0: block (warp + i*8) into stage of (cnt + i)
-    const int b = warp + i * kWarps;
-    const uint32_t c = cnt + i, s = c % kStages;
-    uint8_t* dst = my_ring + s * G::STAGE;
+  auto issue = [&](int b, uint32_t c) {  // lane 0: block b into the stage of count c
+    const uint32_t s = c % kStages;
+    uint8_t* dst = ring + s * G::STAGE;
     const CUtensorMap *km, *vm;
     int key;
     if (b < nbA) { km = &p.tmv_kp; vm = &p.tmv_vp; key = int(pbase + b * kKB); }
     else { km = &p.tmv_kd; vm = &p.tmv_vd; key = int(dbase + (b - nbA) * kKB); }
-    dev::mbar_arrive_expect_tx(&sh->full[warp][s], 2 * G::BLK);
-    dev::tma_load_3d(dst, km, &sh->full[warp][s], 0, it.h, key);
-    dev::tma_load_3d(dst + G::BLK, vm, &sh->full[warp][s], 0, it.h, key);
+    dev::mbar_arrive_expect_tx(&full[s], 2 * G::BLK);
+    dev::tma_load_3d(dst, km, &full[s], 0, it.h, key);
+    dev::tma_load_3d(dst + G::BLK, vm, &full[s], 0, it.h, key);
   };
-
-  float* sm_o = reinterpret_cast<float*>(ring);        // merge area (after the loop)
-  float* sm_ml = sm_o + kWarps * kRP * D;
 
   for (int pr = 0; pr < it.nrows; pr += kRP) {
     const int nr = min(kRP, it.nrows - pr);
     if (lane == 0) {
-      dev::fence_proxy_async_smem();  // ring was last touched by generic loads/stores
-      for (int i = 0; i < min(kStages, mine); ++i) issue(i);
+      dev::fence_proxy_async_smem();  // the ring was last read through the generic proxy
+      for (int i = 0; i < min(kStages, nb); ++i) issue(i, cnt + i);
     }
-    // q slice (8 elements) of each row, fp32
     float2 q[kRP][4];
 #pragma unroll
     for (int r = 0; r < kRP; ++r) {
@@ -127,12 +128,11 @@ __device__ __forceinline__ uint32_t vec_item(const KParams& p, const ItemT& it, 
       for (int e = 0; e < 4; ++e) o[r][e] = make_float2(0.f, 0.f);
     float m = -INFINITY, lp = 0.f;  // running max / partial sum of row (lane & 3)
 
-    for (int i = 0; i < mine; ++i) {
-      const int b = warp + i * kWarps;
-      const uint32_t c = cnt + i, s = c % kStages;
+    for (int b = 0; b < nb; ++b) {
+      const uint32_t c = cnt + b, s = c % kStages;
       const int nvalid = b < nbA ? min(kKB, npA - b * kKB) : min(kKB, npB - (b - nbA) * kKB);
-      dev::mbar_wait(&sh->full[warp][s], (c / kStages) & 1);
-      const uint8_t* kb = my_ring + s * G::STAGE;
+      dev::mbar_wait(&full[s], (c / kStages) & 1);
+      const uint8_t* kb = ring + s * G::STAGE;
       const uint8_t* vb = kb + G::BLK;
       // ---- scores: partial dots for (J key slots x 4 rows), then reduce-scatter
       float v[G::LPK];
@@ -184,11 +184,11 @@ __device__ __forceinline__ uint32_t vec_item(const KParams& p, const ItemT& it, 
         }
       }
       // ---- P V
-      sh->p[warp][lane] = pe;
+      pscratch[lane] = pe;
       __syncwarp();
 #pragma unroll
       for (int j = 0; j < G::J; ++j) {
-        const float4 pj = *reinterpret_cast<const float4*>(&sh->p[warp][kg * G::LPK + j * 4]);
+        const float4 pj = *reinterpret_cast<const float4*>(&pscratch[kg * G::LPK + j * 4]);
         const uint4 w = *reinterpret_cast<const uint4*>(vb + (j * G::KPI + kg) * (D * 2) + ds * 16);
         const float2 v0 = unpack2<T>(w.x), v1 = unpack2<T>(w.y), v2 = unpack2<T>(w.z),
                      v3 = unpack2<T>(w.w);
@@ -203,14 +203,14 @@ __device__ __forceinline__ uint32_t vec_item(const KParams& p, const ItemT& it, 
         }
       }
       __syncwarp();  // stage s and the p scratch are free
-      if (lane == 0 && i + kStages < mine) {
+      if (lane == 0 && b + kStages < nb) {
         dev::fence_proxy_async_smem();
-        issue(i + kStages);
+        issue(b + kStages, c + kStages);
       }
     }
-    cnt += mine;
+    cnt += nb;
 
-    // ---- warp state: sum o over key slots, l over lanes of the same row
+    // ---- finish the rows: sum o over key slots, l over lanes of the same row
 #pragma unroll
     for (int off = G::LPK; off < 32; off <<= 1)
 #pragma unroll
@@ -223,50 +223,16 @@ __device__ __forceinline__ uint32_t vec_item(const KParams& p, const ItemT& it, 
     lp += __shfl_xor_sync(0xffffffffu, lp, 4);
     lp += __shfl_xor_sync(0xffffffffu, lp, 8);
     lp += __shfl_xor_sync(0xffffffffu, lp, 16);
-    __syncthreads();  // every warp is done with its ring: reuse it as the merge area
-    if (kg == 0) {
 #pragma unroll
-      for (int r = 0; r < kRP; ++r) {
-        float4* dst = reinterpret_cast<float4*>(sm_o + (warp * kRP + r) * D + ds * 8);
-        dst[0] = make_float4(o[r][0].x, o[r][0].y, o[r][1].x, o[r][1].y);
-        dst[1] = make_float4(o[r][2].x, o[r][2].y, o[r][3].x, o[r][3].y);
+    for (int r = 0; r < kRP; ++r) {
+      const float M = __shfl_sync(0xffffffffu, m, r);
+      const float L = __shfl_sync(0xffffffffu, lp, r);
+      if (kg == 0 && r < nr) {
+        const float ov[8] = {o[r][0].x, o[r][0].y, o[r][1].x, o[r][1].y,
+                             o[r][2].x, o[r][2].y, o[r][3].x, o[r][3].y};
+        emit8(pr + r, ds * 8, M, L, ov);
       }
     }
-    if (lane < kRP) {
-      sm_ml[(warp * kRP + lane) * 2 + 0] = m;
-      sm_ml[(warp * kRP + lane) * 2 + 1] = mine > 0 ? lp : 0.f;
-    }
-    __syncthreads();
-    // per-row statistics and per-warp factors once, then 4 columns per thread
-    if (threadIdx.x < nr) {
-      const int r = threadIdx.x;
-      float M = -INFINITY;
-#pragma unroll
-      for (int w = 0; w < kWarps; ++w) M = fmaxf(M, sm_ml[(w * kRP + r) * 2]);
-      float Ls = 0.f;
-#pragma unroll
-      for (int w = 0; w < kWarps; ++w) {
-        const float lw = sm_ml[(w * kRP + r) * 2 + 1];
-        const float f = lw > 0.f ? exp2f(sm_ml[(w * kRP + r) * 2] - M) : 0.f;
-        s_f[w * kRP + r] = f;
-        Ls += f * lw;
-      }
-      s_M[r] = M;
-      s_L[r] = Ls;
-    }
-    __syncthreads();
-    for (int idx = threadIdx.x; idx < nr * (D / 4); idx += kWarps * 32) {
-      const int r = idx / (D / 4), c = (idx - r * (D / 4)) * 4;
-      float4 O = make_float4(0.f, 0.f, 0.f, 0.f);
-#pragma unroll
-      for (int w = 0; w < kWarps; ++w) {
-        const float f = s_f[w * kRP + r];
-        const float4 v = *reinterpret_cast<const float4*>(sm_o + (w * kRP + r) * D + c);
-        O.x += f * v.x; O.y += f * v.y; O.z += f * v.z; O.w += f * v.w;
-      }
-      emit4(pr + r, c, s_M[r], s_L[r], O);
-    }
-    __syncthreads();
   }
   return cnt;
 }

@@ -210,6 +210,19 @@ class PrefixSharedAttention:
             _raise_native(st, "psa_run")
         return partial if partial is not None else out
 
+    def trace(self, *inputs) -> np.ndarray:
+        """Run once with per-item timing on (diagnostics). Returns int64 [items, 4]:
+        (cta | smid << 32, kind, t_start_ns, t_end_ns), rows in queue order."""
+        n = self.num_items
+        buf = torch.zeros((n, 4), dtype=torch.int64, device=self.device)
+        L.check(L.lib().psa_debug_set_trace(_ptr(buf), n), "psa_debug_set_trace")
+        try:
+            self(*inputs)
+            torch.cuda.synchronize(self.device)
+        finally:
+            L.lib().psa_debug_set_trace(None, 0)
+        return buf.cpu().numpy()
+
     def device_error(self) -> int:
         """Error bits of the last run (synchronises the current stream)."""
         bits = C.c_int32()

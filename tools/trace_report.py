@@ -1,0 +1,86 @@
+#!/usr/bin/env python
+"""Per-work-item timeline of one persistent launch (diagnostics).
+
+    python tools/trace_report.py --config c2 [--warmup 3] [--json out.json]
+
+Uses psa_debug_set_trace (include/psa.h): every item records its CTA, SM,
+kind and %globaltimer start/end. Reports per-kind counts and durations, CTA
+busy fraction, launch span and the tail after the first CTA ran dry.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import sys
+
+import numpy as np
+import torch
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+
+from paper_2412_03594_b200 import packed as P  # noqa: E402
+from paper_2412_03594_b200 import workloads as W  # noqa: E402
+
+
+def report(tr: np.ndarray, tables: dict) -> dict:
+    cta = (tr[:, 0] & 0xFFFFFFFF).astype(np.int64)
+    kind = tr[:, 1]
+    t0, t1 = tr[:, 2], tr[:, 3]
+    start = t0.min()
+    span = (t1.max() - start) / 1e3
+    dur = (t1 - t0) / 1e3
+    out = {"items": int(len(tr)), "span_us": float(span)}
+    items = tables["items"]
+    keys = (items[:, 7] - items[:, 6]) + (items[:, 9] - items[:, 8])
+    for k, name in ((0, "vec"), (1, "tile")):
+        sel = kind == k
+        if sel.any():
+            out[name] = {"n": int(sel.sum()), "sum_us": float(dur[sel].sum()),
+                         "mean_us": float(dur[sel].mean()), "p50_us": float(np.median(dur[sel])),
+                         "max_us": float(dur[sel].max()),
+                         "keys_mean": float(keys[sel].mean()),
+                         "us_per_1k_keys": float(dur[sel].sum() / keys[sel].sum() * 1e3)}
+    busy = np.bincount(cta, weights=dur)
+    last_end = np.zeros(cta.max() + 1)
+    np.maximum.at(last_end, cta, (t1 - start) / 1e3)
+    out["cta_busy_frac_mean"] = float(busy.mean() / span)
+    out["first_cta_idle_us"] = float(last_end.min())
+    out["tail_us"] = float(span - last_end.min())
+    gaps = []
+    order = np.lexsort((t0, cta))
+    c_s, t0_s, t1_s = cta[order], t0[order], t1[order]
+    same = c_s[1:] == c_s[:-1]
+    gaps = (t0_s[1:] - t1_s[:-1])[same] / 1e3
+    out["gap_between_items_us_mean"] = float(gaps.mean()) if len(gaps) else 0.0
+    return out
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--config", default="c2")
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--json")
+    args = ap.parse_args()
+    dev = torch.device("cuda", 0)
+    spec = W.config(args.config)
+    b = W.make_batch(spec, dev)
+    op = P.PrefixSharedAttention(b["cu_req"], b["cu_q"], b["cu_prefix"], b["cu_distinct"],
+                                 spec.Hq, spec.Hkv, spec.d, spec.dv, spec.torch_dtype, dev)
+    inputs = (b["q"], b["k_prefix"], b["v_prefix"], b["k_distinct"], b["v_distinct"])
+    for _ in range(args.warmup):
+        op(*inputs)
+    torch.cuda.synchronize()
+    tr = op.trace(*inputs)
+    rep = report(tr, op.plan_tables())
+    rep["config"] = args.config
+    print(json.dumps(rep, indent=1))
+    if args.json:
+        with open(args.json, "w") as f:
+            json.dump(rep, f, indent=1)
+        np.save(args.json.replace(".json", ".npy"), tr)
+
+
+if __name__ == "__main__":
+    main()
