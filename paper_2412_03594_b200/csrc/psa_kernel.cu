@@ -652,6 +652,9 @@ __global__ void __launch_bounds__(kThreads, 2) psa_persistent(const __grid_const
   } else {
     cta_phase(p.num_items);
   }
+  // Every warp of this CTA must be done pulling from the queues before the CTA
+  // counts itself out: the last CTA out resets the cursors for the next launch.
+  __syncthreads();
   if (threadIdx.x == 0) {
     __threadfence();
     if (atomicAdd(&p.ctrl->done, 1) == (int)gridDim.x - 1) {

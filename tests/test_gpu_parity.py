@@ -77,6 +77,29 @@ def test_repeat_launches_are_bit_identical_and_reset_counters():
     assert ctrl[0].item() == 0 and ctrl[1].item() == 0
 
 
+@pytest.mark.parametrize("name", ["c2", "c4"])
+def test_relaunch_with_new_inputs_recomputes_everything(name):
+    """One planned op, several launches with different inputs (and a poisoned
+    output buffer each time): every launch must redo every work item, i.e. the
+    queue cursors and merge counters are reset by the kernel itself."""
+    spec = W.config(name)
+    b = W.make_batch(spec, "cuda")
+    op = P.PrefixSharedAttention(b["cu_req"], b["cu_q"], b["cu_prefix"], b["cu_distinct"],
+                                 spec.Hq, spec.Hkv, spec.d, spec.dv, spec.torch_dtype, "cuda")
+    keys = ("q", "k_prefix", "v_prefix", "k_distinct", "v_distinct")
+    for trial in range(3):
+        if trial:
+            for k in keys:
+                b[k].mul_(-1.0 if k == "v_distinct" else 1.0).add_(0.0)
+            b["q"].copy_(torch.randn_like(b["q"]))
+        out = torch.full((b["q"].shape[0], spec.Hq, spec.dv), float("nan"),
+                         dtype=spec.torch_dtype, device="cuda")
+        op(*(b[k] for k in keys), out=out)
+        torch.cuda.synchronize()
+        assert not torch.isnan(out).any(), f"launch {trial} left rows unwritten"
+        check_sampled_groups(spec, b, out, n_groups=2, n_heads=2, seed=trial)
+
+
 def test_lse_output_matches_oracle():
     spec = [s for s in _manifest() if s["name"] == "gqa4_decode_bf16"][0]
     a = C.make_packed(spec)
