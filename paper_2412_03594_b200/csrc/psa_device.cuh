@@ -71,6 +71,12 @@ __device__ __forceinline__ void tmem_alloc(uint32_t* dst_smem) {  // whole warp
                : "memory");
   asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
 }
+// A CTA of a kernel that contains tcgen05.alloc holds the SM's allocation
+// permit until it relinquishes it; a second CTA is not co-scheduled on that SM
+// before then. CTAs that will not allocate must give the permit up at once.
+__device__ __forceinline__ void tmem_relinquish() {  // whole warp
+  asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+}
 template <uint32_t kCols>
 __device__ __forceinline__ void tmem_dealloc(uint32_t taddr) {  // whole warp
   asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(taddr), "n"(kCols)

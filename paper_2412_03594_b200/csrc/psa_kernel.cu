@@ -22,6 +22,7 @@
 #include <cmath>
 #include <cstdint>
 #include <cstring>
+#include <cstdlib>
 
 #include "../../include/psa.h"
 #include "psa_kernel.h"
@@ -560,6 +561,7 @@ __global__ void __launch_bounds__(kThreads, 2) psa_persistent(const __grid_const
   __shared__ A s_fac[kWarps * 8];
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t t_kernel0 = (p.trace_cap > 0 && threadIdx.x == 0) ? int64_t(globaltimer()) : 0;
   tile::State tst{0u, 0u, 0u};
   const bool tiles = kTiles && p.use_tiles;
   if (kVecFast) {
@@ -572,6 +574,7 @@ __global__ void __launch_bounds__(kThreads, 2) psa_persistent(const __grid_const
     }
     __syncthreads();
   }
+  if (kTiles && !tiles && warp == 5) dev::tmem_relinquish();
   if (tiles) {
     if (threadIdx.x == 0) tile::init_barriers(&s_bar);
     if (warp == 4 && lane == 0) {
@@ -655,6 +658,8 @@ __global__ void __launch_bounds__(kThreads, 2) psa_persistent(const __grid_const
   // Every warp of this CTA must be done pulling from the queues before the CTA
   // counts itself out: the last CTA out resets the cursors for the next launch.
   __syncthreads();
+  if (p.trace_cap > 0 && threadIdx.x == 0)  // per-CTA residency record after the items
+    trace_item(p, p.num_items + int(blockIdx.x), -1, t_kernel0);
   if (threadIdx.x == 0) {
     __threadfence();
     if (atomicAdd(&p.ctrl->done, 1) == (int)gridDim.x - 1) {
@@ -738,6 +743,11 @@ int launch_mode(const KParams& p, int32_t num_sms, int32_t ctas_per_sm, void* st
   const size_t smem = smem_for<T>(p, kMode);
   cudaError_t e = cudaFuncSetAttribute(psa_persistent<T, kMode>,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+  if (e != cudaSuccess) return e;
+  // Two CTAs per SM only fit with the maximum shared-memory carveout.
+  e = cudaFuncSetAttribute(psa_persistent<T, kMode>,
+                           cudaFuncAttributePreferredSharedMemoryCarveout,
+                           int(cudaSharedmemCarveoutMaxShared));
   if (e != cudaSuccess) return e;
   const int grid = num_sms * ctas_per_sm;
   psa_persistent<T, kMode><<<grid, kThreads, smem, static_cast<cudaStream_t>(stream)>>>(p);

@@ -212,8 +212,9 @@ class PrefixSharedAttention:
 
     def trace(self, *inputs) -> np.ndarray:
         """Run once with per-item timing on (diagnostics). Returns int64 [items, 4]:
-        (cta | smid << 32, kind, t_start_ns, t_end_ns), rows in queue order."""
-        n = self.num_items
+        (cta | smid << 32 | warp << 48, kind, t_start_ns, t_end_ns), rows in queue order;
+        rows num_items + b hold CTA b's kernel start/end (kind -1)."""
+        n = self.num_items + 4096  # items, then one residency record per CTA
         buf = torch.zeros((n, 4), dtype=torch.int64, device=self.device)
         L.check(L.lib().psa_debug_set_trace(_ptr(buf), n), "psa_debug_set_trace")
         try:
@@ -221,7 +222,9 @@ class PrefixSharedAttention:
             torch.cuda.synchronize(self.device)
         finally:
             L.lib().psa_debug_set_trace(None, 0)
-        return buf.cpu().numpy()
+        out = buf.cpu().numpy()
+        ctas = out[self.num_items:]
+        return out[:self.num_items], ctas[ctas[:, 1] == -1]
 
     def device_error(self) -> int:
         """Error bits of the last run (synchronises the current stream)."""

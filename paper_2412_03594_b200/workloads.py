@@ -79,7 +79,14 @@ def config(name: str) -> Spec:
     if name == "c5":
         return Spec("c5", 32, 8, 128, 128, "bf16", "normal", [4096] * 1024,
                     [[(1, 256)] * 64 for _ in range(1024)], seed=5)
-    raise ValueError(f"unknown config {name!r} (c1..c5)")
+    # diagnostic halves of c2: the shared-prefix tiles alone / the decode part alone
+    if name == "c2_prefix":
+        return Spec("c2_prefix", 32, 8, 128, 128, "bf16", "normal", [2048] * 16,
+                    [[(1, 0)] * 32 for _ in range(16)], seed=2)
+    if name == "c2_decode":
+        return Spec("c2_decode", 32, 8, 128, 128, "bf16", "normal", [0] * 16,
+                    [[(1, 256)] * 32 for _ in range(16)], seed=2)
+    raise ValueError(f"unknown config {name!r} (c1..c5, c2_prefix, c2_decode)")
 
 
 def offsets(spec: Spec) -> dict:

@@ -72,14 +72,19 @@ def main():
     for _ in range(args.warmup):
         op(*inputs)
     torch.cuda.synchronize()
-    tr = op.trace(*inputs)
+    tr, ctas = op.trace(*inputs)
     rep = report(tr, op.plan_tables())
+    st = tr[:, 2].min()
+    rep["cta_start_us_pct"] = [float(x) for x in np.percentile((ctas[:, 2] - st) / 1e3, [0, 50, 90, 100])]
+    rep["ctas_per_sm"] = float(len(ctas) / max(1, len(np.unique(ctas[:, 0] >> 32))))
+    rep["num_ctas"] = int(len(ctas))
     rep["config"] = args.config
     print(json.dumps(rep, indent=1))
     if args.json:
         with open(args.json, "w") as f:
             json.dump(rep, f, indent=1)
         np.save(args.json.replace(".json", ".npy"), tr)
+        np.save(args.json.replace(".json", "_ctas.npy"), ctas)
 
 
 if __name__ == "__main__":
