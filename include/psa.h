@@ -97,9 +97,9 @@ typedef struct psa_plan_opts {
   int32_t ctas_per_sm;    /* 0 = default (2) */
   int32_t tile_min_rows;  /* stacked rows at which a segment uses tcgen05 tiles (0 = default 32) */
   int32_t disable_tiles;  /* 1 = every item on the CUDA-core path (diagnostics) */
-  int32_t min_chunk_keys; /* 0 = default (256) */
+  int32_t min_chunk_keys; /* tile items: minimum KV chunk, 0 = default (512) */
   int32_t max_chunk_keys; /* 0 = default (16384) */
-  int32_t target_waves;   /* 0 = default (4) */
+  int32_t target_waves;   /* tile items per CTA the chunking aims at, 0 = default (1) */
   int32_t disable_vec_fast; /* 1 = CUDA-core items use the generic path (diagnostics) */
 } psa_plan_opts;
 

@@ -23,6 +23,8 @@ TILE_M = 128
 VEC_ROWS = 8
 CHUNK_ALIGN = 64
 VEC_MAX_KEYS = 512
+VEC_WARPS = 8
+VEC_WAVES = 2
 BYTE_WEIGHT = 356
 VEC_FLOP_WEIGHT = 32
 RIDGE = 257
@@ -49,7 +51,7 @@ def tiles_supported(dtype, d, dv, Hq, Hkv, disable_tiles=0):
 
 def build_plan(G, R, Hq, Hkv, d, dv, dtype, cu_req, cu_q, cu_prefix, cu_distinct,
                num_sms=148, ctas_per_sm=2, tile_min_rows=32, disable_tiles=0,
-               min_chunk_keys=256, max_chunk_keys=16384, target_waves=4):
+               min_chunk_keys=512, max_chunk_keys=16384, target_waves=1):
     """Returns dict(items, units, contribs, workspace_rows, chunk_keys, num_tile_items)."""
     cu_req = [int(x) for x in cu_req]
     cu_q = [int(x) for x in cu_q]
@@ -67,26 +69,29 @@ def build_plan(G, R, Hq, Hkv, d, dv, dtype, cu_req, cu_q, cu_prefix, cu_distinct
     def step_for(kind):
         return tile_rows if kind == KIND_TILE else VEC_ROWS
 
-    total = 0
+    total = {KIND_TILE: 0, KIND_VEC: 0}
     for g in range(G):
         tok0 = cu_q[cu_req[g]]
         Ng = gqa * (cu_q[cu_req[g + 1]] - tok0)
         P = cu_prefix[g + 1] - cu_prefix[g]
         if P > 0:
-            total += _cdiv(Ng, step_for(kind_for(Ng))) * P
+            k = kind_for(Ng)
+            total[k] += _cdiv(Ng, step_for(k)) * P
         for r in range(cu_req[g], cu_req[g + 1]):
             D = cu_distinct[r + 1] - cu_distinct[r]
             nr = gqa * (cu_q[r + 1] - cu_q[r])
             if D > 0:
-                total += _cdiv(nr, step_for(kind_for(nr))) * D
-    total *= Hkv
-    target = max(1, num_sms) * max(1, ctas_per_sm) * max(1, target_waves)
-    chunk = _cdiv(total, target)
+                k = kind_for(nr)
+                total[k] += _cdiv(nr, step_for(k)) * D
+    ctas = max(1, num_sms) * max(1, ctas_per_sm)
+    chunk = _cdiv(total[KIND_TILE] * Hkv, ctas * max(1, target_waves))
     chunk = min(max(chunk, min_chunk_keys), max_chunk_keys)
     chunk = _rup(max(chunk, 1), CHUNK_ALIGN)
+    vchunk = _cdiv(total[KIND_VEC] * Hkv, ctas * VEC_WARPS * VEC_WAVES)
+    vchunk = _rup(min(max(vchunk, CHUNK_ALIGN), VEC_MAX_KEYS), CHUNK_ALIGN)
 
     def per(L, kind):
-        ck = chunk if kind == KIND_TILE else min(chunk, VEC_MAX_KEYS)
+        ck = chunk if kind == KIND_TILE else vchunk
         n = _cdiv(L, ck)
         return _rup(_cdiv(L, n), CHUNK_ALIGN)
 

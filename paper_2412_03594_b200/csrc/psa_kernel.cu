@@ -443,12 +443,23 @@ __device__ __forceinline__ void merge_row_warp(const KParams& p, int u, int r) {
     L = L * fo + lsum;
     O.x *= fo; O.y *= fo; O.z *= fo; O.w *= fo;
     M = mn;
-    for (int i = 0; i < n; ++i) {
-      const float fi = __shfl_sync(0xffffffffu, f, i);
-      const int64_t wi = __shfl_sync(0xffffffffu, wr, i);
-      if (fi != 0.f && c < dv) {
-        const float4 v = __ldcg(reinterpret_cast<const float4*>(WO + wi * dv + c));
-        O.x += fi * v.x; O.y += fi * v.y; O.z += fi * v.z; O.w += fi * v.w;
+    // 8 contributions per batch: all loads in flight before the first FMA
+    for (int i0 = 0; i0 < n; i0 += 8) {
+      float4 v[8];
+      float fi[8];
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const int i = i0 + j;
+        fi[j] = __shfl_sync(0xffffffffu, f, i & 31);
+        const int64_t wi = __shfl_sync(0xffffffffu, wr, i & 31);
+        v[j] = (i < n && fi[j] != 0.f && c < dv)
+                   ? __ldcg(reinterpret_cast<const float4*>(WO + wi * dv + c))
+                   : make_float4(0.f, 0.f, 0.f, 0.f);
+        if (i >= n) fi[j] = 0.f;
+      }
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        O.x += fi[j] * v[j].x; O.y += fi[j] * v[j].y; O.z += fi[j] * v[j].z; O.w += fi[j] * v[j].w;
       }
     }
   }

@@ -91,28 +91,40 @@ std::string build_plan(const PlanInput& in, const PlanOptions& opt, Plan* out) {
   };
   auto step_for = [&](int32_t kind) -> int64_t { return kind == kItemTile ? tile_rows : kVecRows; };
 
-  // 1. Chunk size from the total (row block x key) volume.
-  int64_t total = 0;
+  // 1. Chunk sizes from the (row block x key) volume of each item kind.
+  //    TILE items (CTA-level) aim at target_waves waves over all CTAs: every tile
+  //    item writes a 128-row fp32 partial, so fewer, longer tiles are cheaper.
+  //    VEC items (warp-level) aim at kVecWaves waves over all warps, capped at
+  //    kVecMaxKeys keys so a long segment spreads over many warps.
+  int64_t total_tile = 0, total_vec = 0;
   for (int32_t g = 0; g < in.G; ++g) {
     const int64_t tok0 = in.cu_q[in.cu_req[g]];
     const int64_t Ng = gqa * (in.cu_q[in.cu_req[g + 1]] - tok0);
     const int64_t P = in.cu_prefix[g + 1] - in.cu_prefix[g];
-    if (P > 0) total += ceil_div(Ng, step_for(kind_for(Ng))) * P;
+    if (P > 0) {
+      const int32_t k = kind_for(Ng);
+      (k == kItemTile ? total_tile : total_vec) += ceil_div(Ng, step_for(k)) * P;
+    }
     for (int64_t r = in.cu_req[g]; r < in.cu_req[g + 1]; ++r) {
       const int64_t D = in.cu_distinct[r + 1] - in.cu_distinct[r];
       const int64_t nr = gqa * (in.cu_q[r + 1] - in.cu_q[r]);
-      if (D > 0) total += ceil_div(nr, step_for(kind_for(nr))) * D;
+      if (D > 0) {
+        const int32_t k = kind_for(nr);
+        (k == kItemTile ? total_tile : total_vec) += ceil_div(nr, step_for(k)) * D;
+      }
     }
   }
-  total *= in.Hkv;
-  const int64_t target = int64_t(std::max(1, opt.num_sms)) * std::max(1, opt.ctas_per_sm) *
-                         std::max(1, opt.target_waves);
-  int64_t chunk = ceil_div(total, target);
+  total_tile *= in.Hkv;
+  total_vec *= in.Hkv;
+  const int64_t ctas = int64_t(std::max(1, opt.num_sms)) * std::max(1, opt.ctas_per_sm);
+  int64_t chunk = ceil_div(total_tile, ctas * std::max(1, opt.target_waves));
   chunk = std::min<int64_t>(std::max<int64_t>(chunk, opt.min_chunk_keys), opt.max_chunk_keys);
   chunk = round_up(std::max<int64_t>(chunk, 1), kChunkAlign);
+  int64_t vchunk = ceil_div(total_vec, ctas * kVecWarps * kVecWaves);
+  vchunk = std::min<int64_t>(std::max<int64_t>(vchunk, kChunkAlign), kVecMaxKeys);
+  vchunk = round_up(vchunk, kChunkAlign);
   const Chunking ck{chunk};
-  // One warp streams a VEC item: cap its keys so long segments spread over warps.
-  const Chunking ckv{std::min<int64_t>(chunk, kVecMaxKeys)};
+  const Chunking ckv{vchunk};
   out->chunk_keys = int32_t(chunk);
 
   // 2. Canonical items and merge units.

@@ -34,6 +34,8 @@ constexpr int32_t kTileM = 128;        // tcgen05 M (rows per tile)
 constexpr int32_t kVecRows = 8;        // rows per CUDA-core item
 constexpr int32_t kChunkAlign = 64;    // KV chunk boundaries align to 64 keys
 constexpr int64_t kVecMaxKeys = 512;   // warp-level VEC items: at most 512 keys each
+constexpr int64_t kVecWarps = 8;       // warps per CTA that pull VEC items
+constexpr int64_t kVecWaves = 2;       // VEC items per warp the chunking aims at
 constexpr int64_t kByteWeight = 356;   // ~ (tensor FLOP/clk/SM) / (HBM B/clk/SM)
 constexpr int64_t kVecFlopWeight = 32; // tensor / CUDA-core FLOP rate per SM
 constexpr int64_t kRidge = 257;        // measured B200 ridge (FLOP/B) for group costs
@@ -51,9 +53,9 @@ struct PlanOptions {
   int32_t ctas_per_sm = 2;
   int32_t tile_min_rows = 32;
   int32_t disable_tiles = 0;
-  int32_t min_chunk_keys = 256;
+  int32_t min_chunk_keys = 512;
   int32_t max_chunk_keys = 16384;
-  int32_t target_waves = 4;
+  int32_t target_waves = 1;
 };
 
 struct Plan {

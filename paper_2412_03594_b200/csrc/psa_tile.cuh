@@ -9,15 +9,22 @@
 //
 // Per CTA (256 threads) the roles are:
 //   warps 0-3  softmax + epilogue: thread t owns row t == TMEM lane t
-//   warp 4     TMA producer (one lane): Q tile once, K/V blocks into a 2-stage ring
-//   warp 5     MMA issuer (one lane): S = Q K^T and O += P V with tcgen05.mma
-// TMEM (256 columns per CTA, 2 CTAs/SM): S at columns [0, 64), O at [128, 128+dv).
-// Shared memory (d = dv = 128): Q 32 KB, 2 x (K 16 KB + V 16 KB); the bf16 P
-// block of iteration j is written into K_j's stage once S_j = Q K_j^T is done.
+//   warp 4     TMA producer (one lane): Q tile once, then K and V blocks into
+//              two independent 2-stage rings
+//   warp 5     MMA issuer (one lane): S = Q K^T (A, B from smem) and
+//              O += P V (A = P from TMEM, B = V from smem) with tcgen05.mma
+// TMEM (256 columns per CTA, 2 CTAs/SM): S [0, 64), P (bf16 pairs) [64, 96),
+// O [128, 128+dv). Shared memory (d = dv = 128): Q 32 KB, K 2 x 16 KB,
+// V 2 x 16 KB.
+//
+// Pipelining: a K stage is released as soon as S_j = Q K_j^T has completed and
+// a V stage once O += P_j V_j has, so the producer streams K a block ahead of
+// V and never waits for the softmax; in steady state the MMA issuer never
+// waits on a fresh TMA.
 //
 // Online softmax (attention.py:95-98 per block, merge :101-119 across blocks)
 // runs in base 2 with a lazy rescale: O and l are rescaled only when a row's
-// max grows by more than 2^8, so the common case touches O in TMEM never.
+// max grows by more than 2^8, so the common case never touches O in TMEM.
 #pragma once
 
 #include "psa_device.cuh"
@@ -30,6 +37,7 @@ constexpr int kM = 128;          // rows per tile (UMMA M)
 constexpr int kStages = 2;
 constexpr uint32_t kTmemCols = 256;
 constexpr uint32_t kTmemS = 0;
+constexpr uint32_t kTmemP = 64;
 constexpr uint32_t kTmemO = 128;
 constexpr float kRescaleThreshold = 8.0f;  // log2 units
 
@@ -37,7 +45,8 @@ struct Barriers {
   uint64_t q_full;
   uint64_t k_full[kStages];
   uint64_t v_full[kStages];
-  uint64_t kv_empty[kStages];
+  uint64_t k_empty[kStages];
+  uint64_t v_empty[kStages];
   uint64_t s_full;
   uint64_t s_free;
   uint64_t p_full[kStages];  // per stage so a fast softmax can never lap the MMA waiter
@@ -52,9 +61,8 @@ struct State {
 };
 
 __host__ __device__ constexpr size_t smem_bytes(int d, int dv) {
-  // Q + stages*(K+V) (+ separate P when it cannot alias a K stage) + 1 KB alignment slack
-  return size_t(kM) * d * 2 + size_t(kStages) * kBN * (d + dv) * 2 +
-         (d == 128 ? 0 : size_t(kM) * kBN * 2) + 1024;
+  // Q + stages * (K + V) + 1 KB alignment slack
+  return size_t(kM) * d * 2 + size_t(kStages) * kBN * (d + dv) * 2 + 1024;
 }
 
 __device__ __forceinline__ void init_barriers(Barriers* b) {
@@ -62,11 +70,12 @@ __device__ __forceinline__ void init_barriers(Barriers* b) {
   for (int s = 0; s < kStages; ++s) {
     dev::mbar_init(&b->k_full[s], 1);
     dev::mbar_init(&b->v_full[s], 1);
-    dev::mbar_init(&b->kv_empty[s], 1);
+    dev::mbar_init(&b->k_empty[s], 1);
+    dev::mbar_init(&b->v_empty[s], 1);
+    dev::mbar_init(&b->p_full[s], 4);
   }
   dev::mbar_init(&b->s_full, 1);
   dev::mbar_init(&b->s_free, 4);
-  for (int s = 0; s < kStages; ++s) dev::mbar_init(&b->p_full[s], 4);
   dev::mbar_init(&b->o_done, 1);
   dev::fence_mbar_init();
 }
@@ -76,14 +85,12 @@ __device__ __forceinline__ void init_barriers(Barriers* b) {
 struct Layout {
   uint8_t* base;     // 1024-aligned
   uint32_t q_bytes;  // kM * d * 2
-  uint32_t stage;    // K + V bytes of one stage
   uint32_t k_bytes;  // kBN * d * 2
-  uint32_t p_off;    // offset of the separate P buffers (d != 128), else 0
+  uint32_t v_bytes;  // kBN * dv * 2
   __device__ __forceinline__ uint8_t* q() const { return base; }
-  __device__ __forceinline__ uint8_t* k(uint32_t s) const { return base + q_bytes + s * stage; }
-  __device__ __forceinline__ uint8_t* v(uint32_t s) const { return k(s) + k_bytes; }
-  __device__ __forceinline__ uint8_t* p(uint32_t s) const {
-    return p_off ? base + p_off : k(s);  // P_j aliases K_j's stage when the sizes agree
+  __device__ __forceinline__ uint8_t* k(uint32_t s) const { return base + q_bytes + s * k_bytes; }
+  __device__ __forceinline__ uint8_t* v(uint32_t s) const {
+    return base + q_bytes + kStages * k_bytes + s * v_bytes;
   }
 };
 
@@ -93,8 +100,7 @@ __device__ __forceinline__ Layout carve(uint8_t* smem_raw, int d, int dv) {
                                       ~uintptr_t(1023));
   L.q_bytes = kM * d * 2;
   L.k_bytes = kBN * d * 2;
-  L.stage = L.k_bytes + kBN * dv * 2;
-  L.p_off = (d == 128) ? 0u : L.q_bytes + kStages * L.stage;
+  L.v_bytes = kBN * dv * 2;
   return L;
 }
 
@@ -138,6 +144,18 @@ __device__ __forceinline__ Block block_at(const KParams& p, const ItemT& it, int
   return b;
 }
 
+// Diagnostics: clock64 timestamps of the first tile item of CTA 0, written after
+// the trace records (psa_debug_set_trace). Slot = event * 64 + block.
+enum DbgEvent { kEvProdIssue = 0, kEvSIssue, kEvSoftWait, kEvPArrive, kEvPvIssue, kEvMisc,
+                kEvKWaitStart, kEvVWaitStart, kEvVIssue };
+__device__ __forceinline__ void dbg_event(const KParams& p, const State& st, int ev, int n) {
+  if (p.trace_cap > 0 && blockIdx.x == 0 && st.items == 0 && n < 64) {
+    long long t;
+    asm volatile("mov.u64 %0, %%clock64;" : "=l"(t));
+    p.trace[(int64_t(p.num_items) + 4096) * 4 + ev * 64 + n] = t;
+  }
+}
+
 template <typename T, typename ItemT>
 __device__ __forceinline__ State tile_item(const KParams& p, const ItemT& it, uint8_t* smem_raw,
                                            Barriers* bar, State st) {
@@ -154,6 +172,7 @@ __device__ __forceinline__ State tile_item(const KParams& p, const ItemT& it, ui
   const int tokens_per_tile = kM / gqa;
   const uint32_t k_bytes = kBN * d * 2, v_bytes = kBN * dv * 2;
 
+  if (threadIdx.x == 0) dbg_event(p, st, kEvMisc, 2);
   if (warp == 4) {
     // ---------------- TMA producer ----------------
     if (lane == 0) {
@@ -161,16 +180,31 @@ __device__ __forceinline__ State tile_item(const KParams& p, const ItemT& it, ui
       dev::mbar_arrive_expect_tx(&bar->q_full, uint32_t(tokens_per_tile * gqa) * d * 2);
       for (int c = 0; c < d / 64; ++c)
         dev::tma_load_4d(L.q() + c * (kM * 128), &p.tm_q, &bar->q_full, c * 64, 0, it.h, t_start);
-      for (int jb = 0; jb < nb; ++jb) {
+      auto load_k = [&](int jb) {
         const uint32_t n = base_blk + jb, s = n & 1, ph = (n >> 1) & 1;
-        dev::mbar_wait(&bar->kv_empty[s], ph ^ 1);
         const Block b = block_at(p, it, jb, nbA, pbase, dbase);
+        dbg_event(p, st, kEvKWaitStart, jb);
+        dev::mbar_wait(&bar->k_empty[s], ph ^ 1);  // S_{n-2} has consumed this stage
+        dbg_event(p, st, kEvProdIssue, jb);
         dev::mbar_arrive_expect_tx(&bar->k_full[s], k_bytes);
         for (int c = 0; c < d / 64; ++c)
           dev::tma_load_3d(L.k(s) + c * (kBN * 128), b.km, &bar->k_full[s], c * 64, it.h, b.key);
+      };
+      auto load_v = [&](int jb) {
+        const uint32_t n = base_blk + jb, s = n & 1, ph = (n >> 1) & 1;
+        const Block b = block_at(p, it, jb, nbA, pbase, dbase);
+        dbg_event(p, st, kEvVWaitStart, jb);
+        dev::mbar_wait(&bar->v_empty[s], ph ^ 1);  // PV_{n-2} has consumed this stage
+        dbg_event(p, st, kEvVIssue, jb);
         dev::mbar_arrive_expect_tx(&bar->v_full[s], v_bytes);
         for (int c = 0; c < dv / 64; ++c)
           dev::tma_load_3d(L.v(s) + c * (kBN * 128), b.vm, &bar->v_full[s], c * 64, it.h, b.key);
+      };
+      // K runs one block ahead of V: K_{j+1} is requested before V_j.
+      load_k(0);
+      for (int jb = 0; jb < nb; ++jb) {
+        if (jb + 1 < nb) load_k(jb + 1);
+        load_v(jb);
       }
     }
   } else if (warp == 5) {
@@ -179,7 +213,7 @@ __device__ __forceinline__ State tile_item(const KParams& p, const ItemT& it, ui
       constexpr uint32_t fmt = AbFormat<T>::v;
       const uint32_t idesc_s = dev::umma_idesc_f16(fmt, kM, kBN, 0, 0);
       const uint32_t idesc_o = dev::umma_idesc_f16(fmt, kM, uint32_t(dv), 0, 1);
-      const uint32_t tS = st.tmem + kTmemS, tO = st.tmem + kTmemO;
+      const uint32_t tS = st.tmem + kTmemS, tP = st.tmem + kTmemP, tO = st.tmem + kTmemO;
       const uint32_t q_addr = dev::smem_u32(L.q());
       dev::mbar_wait(&bar->q_full, st.items & 1);
       dev::tc_fence_after();
@@ -188,6 +222,7 @@ __device__ __forceinline__ State tile_item(const KParams& p, const ItemT& it, ui
         dev::mbar_wait(&bar->k_full[s], (n >> 1) & 1);
         dev::tc_fence_after();
         const uint32_t k_addr = dev::smem_u32(L.k(s));
+        dbg_event(p, st, kEvSIssue, jb);
         for (int kk = 0; kk < d / 16; ++kk) {
           const uint32_t c = kk >> 2, w = (kk & 3) * 32;
           const uint64_t a = dev::umma_desc_sw128(q_addr + c * (kM * 128) + w, 16, 1024);
@@ -195,6 +230,7 @@ __device__ __forceinline__ State tile_item(const KParams& p, const ItemT& it, ui
           dev::mma_f16_ss(tS, a, b, idesc_s, kk > 0);
         }
         dev::mma_commit(&bar->s_full);
+        dev::mma_commit(&bar->k_empty[s]);
       };
       issue_s(0);
       for (int jb = 0; jb < nb; ++jb) {
@@ -207,14 +243,13 @@ __device__ __forceinline__ State tile_item(const KParams& p, const ItemT& it, ui
         dev::mbar_wait(&bar->p_full[s], (n >> 1) & 1);
         dev::mbar_wait(&bar->v_full[s], (n >> 1) & 1);
         dev::tc_fence_after();
-        const uint32_t p_addr = dev::smem_u32(L.p(s));
         const uint32_t v_addr = dev::smem_u32(L.v(s));
+        dbg_event(p, st, kEvPvIssue, jb);
         for (int kk = 0; kk < kBN / 16; ++kk) {
-          const uint64_t a = dev::umma_desc_sw128(p_addr + kk * 32, 16, 1024);
           const uint64_t b = dev::umma_desc_sw128(v_addr + kk * (16 * 128), kBN * 128, 1024);
-          dev::mma_f16_ss(tO, a, b, idesc_o, (jb > 0 || kk > 0));
+          dev::mma_f16_ts(tO, tP + kk * 8, b, idesc_o, (jb > 0 || kk > 0));
         }
-        dev::mma_commit(&bar->kv_empty[s]);
+        dev::mma_commit(&bar->v_empty[s]);
         dev::mma_commit(&bar->o_done);
       }
     }
@@ -222,13 +257,15 @@ __device__ __forceinline__ State tile_item(const KParams& p, const ItemT& it, ui
     // ---------------- softmax + epilogue (row = threadIdx.x) ----------------
     const int row = threadIdx.x;
     const uint32_t lane_base = uint32_t(warp * 32) << 16;
-    const uint32_t tS = st.tmem + kTmemS + lane_base, tO = st.tmem + kTmemO + lane_base;
+    const uint32_t tS = st.tmem + kTmemS + lane_base, tP = st.tmem + kTmemP + lane_base;
+    const uint32_t tO = st.tmem + kTmemO + lane_base;
     const float sc = float(p.scale) * 1.4426950408889634f;
     float m = -INFINITY, l = 0.f;
     for (int jb = 0; jb < nb; ++jb) {
       const uint32_t n = base_blk + jb, s = n & 1;
       const Block b = block_at(p, it, jb, nbA, pbase, dbase);
       dev::mbar_wait(&bar->s_full, n & 1);
+      if (threadIdx.x == 0) dbg_event(p, st, kEvSoftWait, jb);
       dev::tc_fence_after();
       uint32_t r0[32], r1[32];
       dev::tmem_ld32(tS, r0);
@@ -262,36 +299,31 @@ __device__ __forceinline__ State tile_item(const KParams& p, const ItemT& it, ui
         rescale = true;
       }
       l *= alpha;
-      if (d != 128 && jb > 0) {
-        // separate single P buffer: PV_{n-1} must have finished reading it
-        dev::mbar_wait(&bar->o_done, (n - 1) & 1);
-      }
-      // P row (bf16) into the K-major SW128 layout: 16-byte chunk c of row r at
-      // r*128 + ((c ^ (r & 7)) * 16).
-      uint8_t* prow = L.p(s) + row * 128;
+      // P_n (bf16 pairs) replaces S_n's registers in place: r0[i] = pack(p_2i, p_2i+1).
       const float nm = -m;
 #pragma unroll
-      for (int c = 0; c < kBN / 8; ++c) {
-        float e[8];
-#pragma unroll
-        for (int i = 0; i < 8; ++i) {
-          const int k = c * 8 + i;
-          const float raw = __uint_as_float(k < 32 ? r0[k] : r1[k - 32]);
-          e[i] = exp2f(fmaf(raw, sc, nm));
-          l += e[i];
-        }
-        uint4 v;
-        v.x = pack2<T>(e[0], e[1]);
-        v.y = pack2<T>(e[2], e[3]);
-        v.z = pack2<T>(e[4], e[5]);
-        v.w = pack2<T>(e[6], e[7]);
-        *reinterpret_cast<uint4*>(prow + ((c ^ (row & 7)) * 16)) = v;
+      for (int i = 0; i < 16; ++i) {
+        const float e0 = exp2f(fmaf(__uint_as_float(r0[2 * i]), sc, nm));
+        const float e1 = exp2f(fmaf(__uint_as_float(r0[2 * i + 1]), sc, nm));
+        l += e0 + e1;
+        r0[i] = pack2<T>(e0, e1);
       }
-      if (__any_sync(0xffffffffu, rescale)) {
-        // O holds PV_0..PV_{n-1}: wait for the last one, then scale rows in place
-        // (before signalling p_full, so PV_n accumulates onto the rescaled O).
+#pragma unroll
+      for (int i = 0; i < 16; ++i) {
+        const float e0 = exp2f(fmaf(__uint_as_float(r1[2 * i]), sc, nm));
+        const float e1 = exp2f(fmaf(__uint_as_float(r1[2 * i + 1]), sc, nm));
+        l += e0 + e1;
+        r0[16 + i] = pack2<T>(e0, e1);
+      }
+      // P TMEM and O are read by PV_{n-1}: it must be complete before we overwrite
+      // P or rescale O.
+      if (jb > 0) {
         dev::mbar_wait(&bar->o_done, (n - 1) & 1);
         dev::tc_fence_after();
+      }
+      dev::tmem_st32(tP, r0);
+      if (__any_sync(0xffffffffu, rescale)) {
+        // O holds PV_0..PV_{n-1}: scale rows in place before PV_n accumulates.
         for (int c = 0; c < dv; c += 32) {
           uint32_t o[32];
           dev::tmem_ld32(tO + c, o);
@@ -300,13 +332,14 @@ __device__ __forceinline__ State tile_item(const KParams& p, const ItemT& it, ui
           for (int i = 0; i < 32; ++i) o[i] = __float_as_uint(__uint_as_float(o[i]) * alpha);
           dev::tmem_st32(tO + c, o);
         }
-        dev::tmem_wait_st();
       }
-      dev::fence_proxy_async_smem();
+      dev::tmem_wait_st();
       dev::tc_fence_before();
       __syncwarp();
       if (lane == 0) dev::mbar_arrive(&bar->p_full[s]);
+      if (threadIdx.x == 0) dbg_event(p, st, kEvPArrive, jb);
     }
+    if (threadIdx.x == 0) dbg_event(p, st, kEvMisc, 0);
     // ---------------- epilogue ----------------
     dev::mbar_wait(&bar->o_done, (base_blk + nb - 1) & 1);
     dev::tc_fence_after();
@@ -369,6 +402,7 @@ __device__ __forceinline__ State tile_item(const KParams& p, const ItemT& it, ui
       }
     }
   }
+  if (threadIdx.x == 0) dbg_event(p, st, kEvMisc, 1);
   st.blocks += nb;
   st.items += 1;
   return st;

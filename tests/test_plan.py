@@ -31,9 +31,9 @@ def _compare(off, Hq, Hkv, d, dv, dt, **opt):
                          num_sms=opts.num_sms, ctas_per_sm=opts.ctas_per_sm or 2,
                          tile_min_rows=opts.tile_min_rows or 32,
                          disable_tiles=opts.disable_tiles,
-                         min_chunk_keys=opts.min_chunk_keys or 256,
+                         min_chunk_keys=opts.min_chunk_keys or 512,
                          max_chunk_keys=opts.max_chunk_keys or 16384,
-                         target_waves=opts.target_waves or 4)
+                         target_waves=opts.target_waves or 1)
     assert got["items"].tobytes() == want["items"].tobytes()
     assert got["units"].tobytes() == want["units"].tobytes()
     assert got["contribs"].tobytes() == want["contribs"].tobytes()

@@ -78,6 +78,15 @@ def main():
     rep["cta_start_us_pct"] = [float(x) for x in np.percentile((ctas[:, 2] - st) / 1e3, [0, 50, 90, 100])]
     rep["ctas_per_sm"] = float(len(ctas) / max(1, len(np.unique(ctas[:, 0] >> 32))))
     rep["num_ctas"] = int(len(ctas))
+    ev = getattr(op, "last_tile_events", None)
+    if ev is not None and ev[5, 2] != 0:
+        t0 = ev[5, 2]
+        names = ["prod_issue", "s_issue", "soft_s_ready", "p_arrive", "pv_issue", "misc",
+                 "k_wait_start", "v_wait_start", "v_issue"]
+        nb = int((ev[0] != 0).sum())
+        rep["tile0_events_cycles"] = {nm: [int(x - t0) for x in ev[i, :nb]] for i, nm in enumerate(names) if nm != "misc"}
+        rep["tile0_softmax_end"] = int(ev[5, 0] - t0)
+        rep["tile0_item_end"] = int(ev[5, 1] - t0)
     rep["config"] = args.config
     print(json.dumps(rep, indent=1))
     if args.json:
