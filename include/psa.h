@@ -100,7 +100,8 @@ typedef struct psa_plan_opts {
   int32_t min_chunk_keys; /* tile items: minimum KV chunk, 0 = default (512) */
   int32_t max_chunk_keys; /* 0 = default (16384) */
   int32_t target_waves;   /* tile items per CTA the chunking aims at, 0 = default (1) */
-  int32_t disable_vec_fast; /* 1 = CUDA-core items use the generic path (diagnostics) */
+  int32_t disable_vec_fast; /* 1 = VEC items on the generic CUDA-core path, 2 = on the warp-level
+                               CUDA-core decode path instead of tcgen05 (diagnostics) */
 } psa_plan_opts;
 
 /* Read-only view of a plan's int32 tables (bit-exact with oracle/plan.py). */

@@ -69,25 +69,49 @@ def build_plan(G, R, Hq, Hkv, d, dv, dtype, cu_req, cu_q, cu_prefix, cu_distinct
     def step_for(kind):
         return tile_rows if kind == KIND_TILE else VEC_ROWS
 
-    total = {KIND_TILE: 0, KIND_VEC: 0}
+    total_vec = 0
+    tile_segs = []  # (row blocks x Hkv, keys)
     for g in range(G):
         tok0 = cu_q[cu_req[g]]
         Ng = gqa * (cu_q[cu_req[g + 1]] - tok0)
         P = cu_prefix[g + 1] - cu_prefix[g]
         if P > 0:
             k = kind_for(Ng)
-            total[k] += _cdiv(Ng, step_for(k)) * P
+            blocks = _cdiv(Ng, step_for(k))
+            if k == KIND_TILE:
+                tile_segs.append((blocks * Hkv, P))
+            else:
+                total_vec += blocks * P
         for r in range(cu_req[g], cu_req[g + 1]):
             D = cu_distinct[r + 1] - cu_distinct[r]
             nr = gqa * (cu_q[r + 1] - cu_q[r])
             if D > 0:
                 k = kind_for(nr)
-                total[k] += _cdiv(nr, step_for(k)) * D
+                blocks = _cdiv(nr, step_for(k))
+                if k == KIND_TILE:
+                    tile_segs.append((blocks * Hkv, D))
+                else:
+                    total_vec += blocks * D
     ctas = max(1, num_sms) * max(1, ctas_per_sm)
-    chunk = _cdiv(total[KIND_TILE] * Hkv, ctas * max(1, target_waves))
-    chunk = min(max(chunk, min_chunk_keys), max_chunk_keys)
-    chunk = _rup(max(chunk, 1), CHUNK_ALIGN)
-    vchunk = _cdiv(total[KIND_VEC] * Hkv, ctas * VEC_WARPS * VEC_WAVES)
+    tile_target = ctas * max(1, target_waves)
+
+    def tile_items(ck):
+        return sum(m * _cdiv(L, ck) for m, L in tile_segs)
+
+    lo = _rup(max(min_chunk_keys, 1), CHUNK_ALIGN)
+    hi = max(lo, _rup(max(max_chunk_keys, 1), CHUNK_ALIGN))
+    if tile_items(lo) > tile_target:
+        while lo < hi:
+            mid = _rup((lo + hi) // 2, CHUNK_ALIGN)
+            if mid >= hi:
+                break
+            if tile_items(mid) <= tile_target:
+                hi = mid
+            else:
+                lo = mid + CHUNK_ALIGN
+        lo = lo if tile_items(lo) <= tile_target else hi
+    chunk = lo
+    vchunk = _cdiv(total_vec * Hkv, ctas * VEC_WARPS * VEC_WAVES)
     vchunk = _rup(min(max(vchunk, CHUNK_ALIGN), VEC_MAX_KEYS), CHUNK_ALIGN)
 
     def per(L, kind):

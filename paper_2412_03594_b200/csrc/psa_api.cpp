@@ -20,6 +20,7 @@ struct psa_plan {
   int32_t num_sms = 0, ctas_per_sm = 0;
   bool use_tiles = false;
   bool use_vec_fast = false;
+  bool use_dec = false;
   std::vector<int64_t> group_tok0, group_pbase, req_dbase;
   int64_t num_tokens = 0, prefix_keys = 0, distinct_keys = 0;
   // workspace layout (byte offsets)
@@ -148,6 +149,8 @@ psa_status psa_plan_create(const psa_problem* prob, const psa_plan_opts* opts, p
   pl->use_tiles = pl->plan.num_tile_items > 0;
   pl->use_vec_fast = psa::vec_fast_supported(prob->dtype, prob->head_dim, prob->value_dim) &&
                      !(opts && opts->disable_vec_fast == 1);
+  pl->use_dec = psa::dec_supported(prob->dtype, prob->head_dim, prob->value_dim) &&
+                !(opts && opts->disable_vec_fast == 2);
   const auto& in = pl->dims;
   pl->group_tok0.resize(in.G);
   pl->group_pbase.resize(in.G);
@@ -258,7 +261,8 @@ psa_status psa_run(const psa_problem* prob, const psa_plan* pl, void* ws, size_t
   k.trace_cap = int32_t(g_trace_cap);
   k.use_tiles = pl->use_tiles ? 1 : 0;
   k.use_vec_fast = (pl->use_vec_fast && !(prob->flags & PSA_FLAG_PARTIAL_OUT)) ? 1 : 0;
-  if (k.use_tiles || k.use_vec_fast) {
+  k.use_dec = (k.use_vec_fast && pl->use_dec) ? 1 : 0;
+  if (k.use_tiles || k.use_vec_fast || k.use_dec) {
     const uintptr_t align = reinterpret_cast<uintptr_t>(prob->q) |
                             reinterpret_cast<uintptr_t>(prob->k_prefix) |
                             reinterpret_cast<uintptr_t>(prob->v_prefix) |

@@ -1,0 +1,453 @@
+// psa_dec.cuh — VEC work items (few query rows vs. a request's distinct KV) on the
+// 5th-gen tensor cores, with the key dimension as the MMA's M.
+//
+// A decode item has <= 16 query rows (the gqa heads of one token, padded) and
+// up to 512 keys — the reference's per-request partial_attention(q_r, dk_r,
+// dv_r) (attention.py:187-189). On CUDA cores it costs ~50 instructions per key;
+// here the dot products run as
+//     S^T[128 keys x 16 rows] = K_blk[128 x d] . Q^T          (A = K, smem)
+//     O^T[dv x 16 rows]      += V_blk^T[dv x 128] . P^T        (A = V^T, MN-major)
+// so the CUDA cores only do the softmax: one thread per key, <= 16 values each.
+//
+// The CTA runs a decoupled, persistent pipeline over the VEC queue:
+//   warp 4   producer: pulls items, stages Q rows, streams K/V blocks into a
+//            3-slot ring of 32 KB slots (K_j, V_j, K_j+1, ...) with TMA,
+//            running ahead into the next item;
+//   warp 5   MMA issuer: polls its two streams (S for the next block, PV for
+//            the oldest finished softmax) and issues whichever is ready;
+//   warps 0-3 softmax + epilogue (thread t = key t of the block; at the end of
+//            an item thread t = value column t).
+// TMEM: S^T [0,16), O^T double buffer [32,48) / [48,64).
+#pragma once
+
+#include "psa_device.cuh"
+
+namespace psa {
+namespace dec {
+
+constexpr int kBK = 128;               // keys per block (MMA M)
+constexpr int kN = 16;                 // query rows per item (MMA N), padded
+constexpr int kR = 8;                  // rows per VEC item (planner kVecRows)
+constexpr int kSlots = 3;              // K/V ring slots
+constexpr int kSlotBytes = kBK * 128 * 2;  // one K or V block, d = 128 bf16 = 32 KB
+constexpr int kQBytes = kN * 128 * 2;  // one item's Q rows = 4 KB
+constexpr int kPBytes = kN * kBK * 2;  // P^T = 4 KB
+constexpr uint32_t kTmemS = 0, kTmemO = 32;
+constexpr float kRescaleThreshold = 8.0f;
+
+__host__ __device__ constexpr size_t smem_bytes() {
+  return size_t(kSlots) * kSlotBytes + 2 * kQBytes + kPBytes + 1024;
+}
+
+struct alignas(16) Shared {
+  uint64_t slot_full[kSlots], slot_empty[kSlots];
+  uint64_t item_full[2], item_empty[2];
+  uint64_t s_full, s_free, p_full[2], o_done, o_full[2], o_empty[2];
+  int item_idx[2];
+  float red[4][kR];   // per-warp partial row maxima / sums
+  // merge queue: softmax thread 0 appends the units this CTA completes, warps 6-7 merge them
+  int mq[64];
+  int mq_tail, mq_head, mq_done, mq_closed;
+};
+
+__device__ __forceinline__ void init_barriers(Shared* s) {
+  for (int i = 0; i < kSlots; ++i) {
+    dev::mbar_init(&s->slot_full[i], 1);
+    dev::mbar_init(&s->slot_empty[i], 1);
+  }
+  for (int i = 0; i < 2; ++i) {
+    dev::mbar_init(&s->item_full[i], 1);
+    dev::mbar_init(&s->item_empty[i], 2);  // MMA (after the item's last S) + softmax epilogue
+    dev::mbar_init(&s->p_full[i], 4);
+    dev::mbar_init(&s->o_full[i], 1);
+    dev::mbar_init(&s->o_empty[i], 4);
+  }
+  dev::mbar_init(&s->s_full, 1);
+  dev::mbar_init(&s->s_free, 4);
+  dev::mbar_init(&s->o_done, 1);
+  s->mq_tail = s->mq_head = s->mq_done = s->mq_closed = 0;
+  dev::fence_mbar_init();
+}
+
+__device__ __forceinline__ int ld_volatile(const int* p) { return *reinterpret_cast<const volatile int*>(p); }
+__device__ __forceinline__ void st_volatile(int* p, int v) { *reinterpret_cast<volatile int*>(p) = v; }
+
+// Softmax thread 0: hand unit u to the merge warps (bounded ring, spins only if 64 are pending).
+__device__ __forceinline__ void enqueue_merge(Shared* sh, int u) {
+  const int tail = sh->mq_tail;
+  while (tail - ld_volatile(&sh->mq_done) >= 64) __nanosleep(64);
+  st_volatile(&sh->mq[tail & 63], u);
+  __threadfence_block();
+  st_volatile(&sh->mq_tail, tail + 1);
+}
+
+// Warps 6-7: merge queued units until the queue is closed and drained.
+template <typename MergeUnit>
+__device__ __forceinline__ void merge_loop(Shared* sh, MergeUnit&& merge_unit) {
+  const int lane = threadIdx.x & 31;
+  for (;;) {
+    int u = -1;
+    if (lane == 0) {
+      const int h = atomicAdd(&sh->mq_head, 1);
+      for (;;) {
+        if (h < ld_volatile(&sh->mq_tail)) { u = ld_volatile(&sh->mq[h & 63]); break; }
+        if (ld_volatile(&sh->mq_closed) && h >= ld_volatile(&sh->mq_tail)) break;
+        __nanosleep(128);
+      }
+    }
+    u = __shfl_sync(0xffffffffu, u, 0);
+    if (u < 0) break;
+    __threadfence();  // acquire: the unit's partials were published before it was queued
+    merge_unit(u);
+    __syncwarp();
+    if (lane == 0) atomicAdd(&sh->mq_done, 1);
+  }
+}
+
+__device__ __forceinline__ void named_sync_softmax() {  // warps 0-3
+  asm volatile("bar.sync 1, 128;" ::: "memory");
+}
+
+struct Geo {
+  uint8_t* base;  // 1024-aligned
+  __device__ __forceinline__ uint8_t* slot(uint32_t i) const { return base + i * kSlotBytes; }
+  __device__ __forceinline__ uint8_t* q(uint32_t i) const {
+    return base + kSlots * kSlotBytes + i * kQBytes;
+  }
+  __device__ __forceinline__ uint8_t* pt() const { return base + kSlots * kSlotBytes + 2 * kQBytes; }
+};
+
+__device__ __forceinline__ Geo carve(uint8_t* smem_raw) {
+  Geo g;
+  g.base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                      ~uintptr_t(1023));
+  return g;
+}
+
+// Byte offset of element (row r, col c) in a K-major SW128 tile with 64-element
+// chunks of `rows` rows: chunk (c / 64), row r, 16-byte unit ((c % 64) / 8) ^ (r % 8).
+__device__ __forceinline__ uint32_t sw128_off(int r, int c, int rows) {
+  return uint32_t((c >> 6) * rows * 128 + r * 128 + ((((c & 63) >> 3) ^ (r & 7)) << 4) +
+                  (c & 7) * 2);
+}
+
+template <typename ItemT>
+__device__ __forceinline__ void item_blocks(const KParams& p, const ItemT& it, int& nbA, int& nb,
+                                            int64_t& pbase, int64_t& dbase) {
+  const int npA = it.pk1 - it.pk0, npB = it.dk1 - it.dk0;
+  nbA = (npA + kBK - 1) / kBK;
+  nb = nbA + (npB + kBK - 1) / kBK;
+  pbase = npA ? __ldg(p.group_pbase + it.g) + it.pk0 : 0;
+  dbase = (it.req >= 0) ? __ldg(p.req_dbase + it.req) + it.dk0 : 0;
+}
+
+template <typename ItemT>
+__device__ __forceinline__ int block_nvalid(const ItemT& it, int nbA, int j) {
+  return j < nbA ? min(kBK, it.pk1 - it.pk0 - j * kBK) : min(kBK, it.dk1 - it.dk0 - (j - nbA) * kBK);
+}
+
+// The decode pipeline. `load(idx)` returns the ItemRec of queue entry idx;
+// `epilogue_out` / `arrive_merge` are provided by the kernel (output + merges).
+template <typename T, typename LoadItem, typename Finish, typename MergeUnit>
+__device__ void run(const KParams& p, uint8_t* smem_raw, Shared* sh, uint32_t tmem,
+                    LoadItem&& load_item_at, Finish&& finish, MergeUnit&& merge_unit) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const Geo G = carve(smem_raw);
+  const int n_items = p.num_items;
+
+  if (warp == 4) {
+    // ================= producer =================
+    uint32_t c = 0;  // K/V slot loads issued
+    for (uint32_t k = 0;; ++k) {
+      const uint32_t q = k & 1;
+      dev::mbar_wait(&sh->item_empty[q], ((k >> 1) & 1) ^ 1);
+      int idx = 0;
+      if (lane == 0) idx = p.n_tile_items + atomicAdd(&p.ctrl->next_vec, 1);
+      idx = __shfl_sync(0xffffffffu, idx, 0);
+      if (idx >= n_items) {
+        if (lane == 0) {
+          sh->item_idx[q] = -1;
+          dev::mbar_arrive(&sh->item_full[q]);
+        }
+        break;
+      }
+      const auto it = load_item_at(idx);
+      // Q rows of the item -> K-major SW128 [16 rows][128] (2 chunks of 64), lane-parallel
+      {
+        const int64_t tok0 = __ldg(p.group_tok0 + it.g);
+        const T* Q = static_cast<const T*>(p.q);
+        uint8_t* qs = G.q(q);
+        for (int u = lane; u < kN * 16; u += 32) {  // 16-byte units: row u/16, unit u%16
+          const int r = u >> 4, cu = u & 15;
+          uint4 v = make_uint4(0u, 0u, 0u, 0u);
+          if (r < it.nrows) {
+            const int row = it.row0 + r;
+            const T* qr = Q + ((tok0 + row / p.gqa) * p.Hq + (int64_t)it.h * p.gqa + row % p.gqa) * 128;
+            v = __ldg(reinterpret_cast<const uint4*>(qr) + cu);
+          }
+          *reinterpret_cast<uint4*>(qs + sw128_off(r, cu * 8, kN)) = v;
+        }
+        dev::fence_proxy_async_smem();
+        __syncwarp();
+      }
+      if (lane == 0) {
+        sh->item_idx[q] = idx;
+        dev::mbar_arrive(&sh->item_full[q]);
+        int nbA, nb;
+        int64_t pbase, dbase;
+        item_blocks(p, it, nbA, nb, pbase, dbase);
+        for (int j = 0; j < nb; ++j) {
+          const CUtensorMap *km, *vm;
+          int key;
+          if (j < nbA) { km = &p.tmd_kp; vm = &p.tmd_vp; key = int(pbase + j * kBK); }
+          else { km = &p.tmd_kd; vm = &p.tmd_vd; key = int(dbase + (j - nbA) * kBK); }
+          for (int w = 0; w < 2; ++w, ++c) {  // K then V
+            const uint32_t s = c % kSlots;
+            dev::mbar_wait(&sh->slot_empty[s], ((c / kSlots) & 1) ^ 1);
+            dev::mbar_arrive_expect_tx(&sh->slot_full[s], kSlotBytes);
+            const CUtensorMap* m = w == 0 ? km : vm;
+            dev::tma_load_3d(G.slot(s), m, &sh->slot_full[s], 0, it.h, key);
+            dev::tma_load_3d(G.slot(s) + kBK * 128, m, &sh->slot_full[s], 64, it.h, key);
+          }
+        }
+      }
+      __syncwarp();
+    }
+  } else if (warp == 5) {
+    // ================= MMA issuer =================
+    if (lane == 0) {
+      constexpr uint32_t fmt = tile::AbFormat<T>::v;
+      const uint32_t idesc_s = dev::umma_idesc_f16(fmt, kBK, kN, 0, 0);
+      const uint32_t idesc_o = dev::umma_idesc_f16(fmt, 128, kN, 1, 0);
+      const uint32_t tS = tmem + kTmemS;
+      const uint32_t pt = dev::smem_u32(G.pt());
+      // S stream: (item k_s, block j_s, global block gS); PV stream lags behind.
+      uint32_t k_s = 0, gS = 0;
+      int j_s = 0, nb_s = -1, nbA_s = 0;
+      uint32_t k_p = 0, gP = 0;
+      int j_p = 0, nb_p = -1;
+      bool s_done = false;
+      int nbs_ring[2] = {0, 0};  // blocks per in-flight item (by k & 1)
+      for (;;) {
+        bool progress = false;
+        // ---- S stream
+        if (!s_done) {
+          const uint32_t q = k_s & 1;
+          if (nb_s < 0 && dev::mbar_test(&sh->item_full[q], (k_s >> 1) & 1)) {
+            const int idx = sh->item_idx[q];
+            if (idx < 0) {
+              s_done = true;
+              nbs_ring[q] = -1;
+            } else {
+              const auto it = load_item_at(idx);
+              int64_t pb, db;
+              item_blocks(p, it, nbA_s, nb_s, pb, db);
+              nbs_ring[q] = nb_s;
+              j_s = 0;
+            }
+            progress = true;
+          }
+          if (nb_s > 0) {
+            const uint32_t cK = 2 * gS, s = cK % kSlots;
+            const bool sfree = gS == 0 || dev::mbar_test(&sh->s_free, (gS - 1) & 1);
+            if (sfree && dev::mbar_test(&sh->slot_full[s], (cK / kSlots) & 1)) {
+              dev::tc_fence_after();
+              const uint32_t a0 = dev::smem_u32(G.slot(s)), b0 = dev::smem_u32(G.q(q));
+              for (int kk = 0; kk < 8; ++kk) {
+                const uint32_t ch = kk >> 2, w = (kk & 3) * 32;
+                const uint64_t a = dev::umma_desc_sw128(a0 + ch * (kBK * 128) + w, 16, 1024);
+                const uint64_t b = dev::umma_desc_sw128(b0 + ch * (kN * 128) + w, 16, 1024);
+                dev::mma_f16_ss(tS, a, b, idesc_s, kk > 0);
+              }
+              dev::mma_commit(&sh->s_full);
+              dev::mma_commit(&sh->slot_empty[s]);
+              ++gS;
+              if (++j_s == nb_s) {
+                dev::mma_commit(&sh->item_empty[q]);  // Q slot reusable once these S complete
+                nb_s = -1;
+                ++k_s;
+              }
+              progress = true;
+            }
+          }
+        }
+        // ---- PV stream
+        if (gP < gS) {
+          const uint32_t q = k_p & 1, b = k_p & 1;
+          if (nb_p < 0) { nb_p = nbs_ring[q]; j_p = 0; }
+          const uint32_t cV = 2 * gP + 1, s = cV % kSlots;
+          const bool need_o = j_p == 0;
+          if (dev::mbar_test(&sh->p_full[gP & 1], (gP >> 1) & 1) &&
+              dev::mbar_test(&sh->slot_full[s], (cV / kSlots) & 1) &&
+              (!need_o || dev::mbar_test(&sh->o_empty[b], ((k_p >> 1) & 1) ^ 1))) {
+            dev::tc_fence_after();
+            const uint32_t a0 = dev::smem_u32(G.slot(s));
+            const uint32_t tO = tmem + kTmemO + b * kN;
+            for (int kk = 0; kk < kBK / 16; ++kk) {
+              const uint64_t a = dev::umma_desc_sw128(a0 + kk * (16 * 128), kBK * 128, 1024);
+              const uint64_t bd = dev::umma_desc_sw128(pt + (kk >> 2) * (kN * 128) + (kk & 3) * 32, 16, 1024);
+              dev::mma_f16_ss(tO, a, bd, idesc_o, (j_p > 0 || kk > 0));
+            }
+            dev::mma_commit(&sh->slot_empty[s]);
+            dev::mma_commit(&sh->o_done);
+            ++gP;
+            if (++j_p == nb_p) {
+              dev::mma_commit(&sh->o_full[b]);
+              nb_p = -1;
+              ++k_p;
+            }
+            progress = true;
+          }
+        }
+        if (s_done && gP == gS) break;
+        (void)progress;
+      }
+    }
+  } else if (warp >= 6) {
+    merge_loop(sh, merge_unit);
+  } else if (warp < 4) {
+    // ================= softmax + epilogue =================
+    const int t = threadIdx.x;
+    const uint32_t lane_base = uint32_t(warp * 32) << 16;
+    const uint32_t tS = tmem + kTmemS + lane_base;
+    const float sc = float(p.scale) * 1.4426950408889634f;
+    uint8_t* pt = G.pt();
+    uint32_t g = 0;  // global block counter
+    for (uint32_t k = 0;; ++k) {
+      const uint32_t q = k & 1, b = k & 1;
+      dev::mbar_wait(&sh->item_full[q], (k >> 1) & 1);
+      const int idx = sh->item_idx[q];
+      if (idx < 0) {
+        if (t == 0) {
+          __threadfence_block();
+          st_volatile(&sh->mq_closed, 1);
+        }
+        break;
+      }
+      long long t_item0 = 0;
+      if (p.trace_cap > 0 && t == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_item0));
+      const auto it = load_item_at(idx);
+      int nbA, nb;
+      int64_t pbase, dbase;
+      item_blocks(p, it, nbA, nb, pbase, dbase);
+      const int R = it.nrows;
+      float m[kR], lp[kR];
+#pragma unroll
+      for (int r = 0; r < kR; ++r) { m[r] = -INFINITY; lp[r] = 0.f; }
+      for (int j = 0; j < nb; ++j, ++g) {
+        const int nvalid = block_nvalid(it, nbA, j);
+        dev::mbar_wait(&sh->s_full, g & 1);
+        dev::tc_fence_after();
+        uint32_t sr[kN];
+        dev::tmem_ld16(tS, sr);
+        dev::tmem_wait_ld();
+        dev::tc_fence_before();
+        __syncwarp();
+        if (lane == 0) dev::mbar_arrive(&sh->s_free);
+        const bool valid = t < nvalid;
+        // block max per row: warp reduce, then across the 4 softmax warps
+        float x[kR];
+#pragma unroll
+        for (int r = 0; r < kR; ++r) {
+          x[r] = (valid && r < R) ? __uint_as_float(sr[r]) * sc : -INFINITY;
+          float v = x[r];
+          if (r < R) {
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
+            if (lane == 0) sh->red[warp][r] = v;
+          }
+        }
+        named_sync_softmax();
+        float alpha[kR];
+        bool any_rescale = false;
+#pragma unroll
+        for (int r = 0; r < kR; ++r) {
+          alpha[r] = 1.f;
+          if (r < R) {
+            const float bm = fmaxf(fmaxf(sh->red[0][r], sh->red[1][r]),
+                                   fmaxf(sh->red[2][r], sh->red[3][r]));
+            if (bm > m[r] + kRescaleThreshold) {  // first block too (m = -inf)
+              alpha[r] = dev::ex2(m[r] - bm);
+              any_rescale |= (m[r] != -INFINITY);
+              m[r] = bm;
+            }
+          }
+        }
+        named_sync_softmax();  // red[] may be rewritten by the next block only after all read it
+        // P^T (single buffer): PV_{g-1} must be done reading it (and O before rescale)
+        if (g > 0) {
+          dev::mbar_wait(&sh->o_done, (g - 1) & 1);
+          dev::tc_fence_after();
+        }
+#pragma unroll
+        for (int r = 0; r < kR; ++r) {
+          if (r < R) {
+            const float e = dev::ex2(x[r] - m[r]);
+            lp[r] = lp[r] * alpha[r] + e;
+            T h;
+            if constexpr (sizeof(T) == 2) h = T(e);
+            *reinterpret_cast<T*>(pt + sw128_off(r, t, kN)) = h;
+          }
+        }
+        if (any_rescale && j > 0) {
+          // O^T lane t (value column t) holds this item's rows as columns
+          const uint32_t tO = tmem + kTmemO + b * kN + lane_base;
+          uint32_t o[kN];
+          dev::tmem_ld16(tO, o);
+          dev::tmem_wait_ld();
+#pragma unroll
+          for (int r = 0; r < kR; ++r) o[r] = __float_as_uint(__uint_as_float(o[r]) * alpha[r]);
+          dev::tmem_st16(tO, o);
+          dev::tmem_wait_st();
+        }
+        dev::fence_proxy_async_smem();
+        dev::tc_fence_before();
+        __syncwarp();
+        if (lane == 0) dev::mbar_arrive(&sh->p_full[g & 1]);
+      }
+      // ---- item end: l per row, then O^T lane t = value column t
+#pragma unroll
+      for (int r = 0; r < kR; ++r) {
+        if (r < R) {
+          float v = lp[r];
+#pragma unroll
+          for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+          if (lane == 0) sh->red[warp][r] = v;
+        }
+      }
+      named_sync_softmax();
+      float L[kR];
+#pragma unroll
+      for (int r = 0; r < kR; ++r)
+        L[r] = r < R ? (sh->red[0][r] + sh->red[1][r]) + (sh->red[2][r] + sh->red[3][r]) : 0.f;
+      dev::mbar_wait(&sh->o_full[b], (k >> 1) & 1);
+      dev::tc_fence_after();
+      uint32_t o[kN];
+      dev::tmem_ld16(tmem + kTmemO + b * kN + lane_base, o);
+      dev::tmem_wait_ld();
+      dev::tc_fence_before();
+      __syncwarp();
+      if (lane == 0) dev::mbar_arrive(&sh->o_empty[b]);
+      float ov[kR];
+#pragma unroll
+      for (int r = 0; r < kR; ++r) ov[r] = __uint_as_float(o[r]);
+      finish(it, t, R, m, L, ov);  // writes output / partial, arrives at merge units
+      named_sync_softmax();        // red[] reuse + item slot release after everyone finished
+      if (t == 0) dev::mbar_arrive(&sh->item_empty[q]);
+      if (p.trace_cap > 0 && t == 0 && idx < p.trace_cap) {
+        long long t1;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1));
+        uint32_t smid;
+        asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+        int64_t* tr = p.trace + int64_t(idx) * 4;
+        tr[0] = int64_t(blockIdx.x) | (int64_t(smid) << 32);
+        tr[1] = 0;
+        tr[2] = t_item0;
+        tr[3] = t1;
+      }
+    }
+  }
+}
+
+}  // namespace dec
+}  // namespace psa

@@ -29,6 +29,7 @@
 #include "psa_plan.h"
 #include "psa_tile.cuh"
 #include "psa_vec.cuh"
+#include "psa_dec.cuh"
 
 namespace psa {
 namespace {
@@ -466,6 +467,107 @@ __device__ __forceinline__ void merge_row_warp(const KParams& p, int u, int r) {
   if (c < dv) write_final4<T>(p, g, h, row0 + r, c, M, L, O);
 }
 
+// Warp merge of rows [r0, r0 + nr) of unit u with nr * cc <= 32 (fp32, dv % 4 == 0,
+// dv <= 128): lane l < nr * cc loads the (m, l) of (row l / cc, contribution
+// l % cc); every o the rows need is then issued before the first FMA, so the
+// whole chunk costs two memory round trips. Combination order per row is the
+// contribution order (bit-reproducible).
+template <typename T>
+__device__ __forceinline__ void merge_chunk_warp(const KParams& p, int u, int r0, int nr) {
+  const int lane = threadIdx.x & 31;
+  const int32_t* U = p.units + (int64_t)u * kUnitWords;
+  const int g = __ldg(U + kUnGroup), h = __ldg(U + kUnHead), row0 = __ldg(U + kUnRow0);
+  const int cb = __ldg(U + kUnContribBegin), cc = __ldg(U + kUnContribCount);
+  const float* WO = static_cast<const float*>(p.ws_o);
+  const float2* WML = static_cast<const float2*>(p.ws_ml);
+  const int dv = p.dv, c = lane * 4;
+  int64_t wr = 0;
+  float2 ml = make_float2(-INFINITY, 0.f);
+  if (lane < nr * cc) {
+    const int r = lane / cc, i = lane - r * cc;
+    wr = (int64_t)__ldg(p.contribs + cb + i) + r0 + r;
+    ml = __ldcg(WML + wr);
+  }
+  const float mv = ml.y > 0.f ? ml.x : -INFINITY;
+  // per-row max over the row's cc lanes (lanes of a row are contiguous)
+  float M = -INFINITY;
+  const int my_r = lane / max(cc, 1);
+  for (int i = 0; i < cc; ++i) M = fmaxf(M, __shfl_sync(0xffffffffu, mv, min(my_r * cc + i, 31)));
+  const float f = ml.y > 0.f ? dev::ex2(ml.x - M) : 0.f;
+  const float fl = f * ml.y;
+  if (cc <= 8) {
+    // groups of rg rows: rg * cc <= 8 (row, contribution) pairs, all loads in flight
+    const int rg = 8 / cc;
+    for (int rb = 0; rb < nr; rb += rg) {
+      const int np = min(rg, nr - rb) * cc;
+      float fi[8];
+      float4 v[8];
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const int src = min(rb * cc + j, 31);
+        fi[j] = j < np ? __shfl_sync(0xffffffffu, f, src) : 0.f;
+        const int64_t wj = __shfl_sync(0xffffffffu, wr, src);
+        v[j] = (j < np && fi[j] != 0.f && c < dv)
+                   ? __ldcg(reinterpret_cast<const float4*>(WO + wj * dv + c))
+                   : make_float4(0.f, 0.f, 0.f, 0.f);
+      }
+      for (int rr = 0; rr < rg && rb + rr < nr; ++rr) {
+        float4 O = make_float4(0.f, 0.f, 0.f, 0.f);
+        float L = 0.f;
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          const bool mine = j >= rr * cc && j < (rr + 1) * cc;
+          const float fj = mine ? fi[j] : 0.f;
+          O.x += fj * v[j].x; O.y += fj * v[j].y; O.z += fj * v[j].z; O.w += fj * v[j].w;
+        }
+        for (int i = 0; i < cc; ++i) L += __shfl_sync(0xffffffffu, fl, min((rb + rr) * cc + i, 31));
+        const float Mr = __shfl_sync(0xffffffffu, M, min((rb + rr) * cc, 31));
+        if (c < dv) write_final4<T>(p, g, h, row0 + r0 + rb + rr, c, Mr, L, O);
+      }
+    }
+    return;
+  }
+  for (int rr = 0; rr < nr; ++rr) {
+    float L = 0.f;
+    float4 O = make_float4(0.f, 0.f, 0.f, 0.f);
+    float fi[8];
+    float4 v[8];
+    for (int i0 = 0; i0 < cc; i0 += 8) {
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const int src = min(rr * cc + i0 + j, 31);
+        const bool ok = i0 + j < cc;
+        fi[j] = ok ? __shfl_sync(0xffffffffu, f, src) : 0.f;
+        const float flj = __shfl_sync(0xffffffffu, fl, src);
+        const int64_t wj = __shfl_sync(0xffffffffu, wr, src);
+        if (ok) L += flj;
+        v[j] = (ok && fi[j] != 0.f && c < dv)
+                   ? __ldcg(reinterpret_cast<const float4*>(WO + wj * dv + c))
+                   : make_float4(0.f, 0.f, 0.f, 0.f);
+      }
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        O.x += fi[j] * v[j].x; O.y += fi[j] * v[j].y; O.z += fi[j] * v[j].z; O.w += fi[j] * v[j].w;
+      }
+    }
+    const float Mr = __shfl_sync(0xffffffffu, M, min(rr * cc, 31));
+    if (c < dv) write_final4<T>(p, g, h, row0 + r0 + rr, c, Mr, L, O);
+  }
+}
+
+// All rows of unit u, by one warp, in chunks of <= 32 (row, contribution) pairs.
+template <typename T>
+__device__ __forceinline__ void merge_unit_warp(const KParams& p, int u) {
+  const int32_t* U = p.units + (int64_t)u * kUnitWords;
+  const int rows = __ldg(U + kUnRows), cc = __ldg(U + kUnContribCount);
+  if (cc > 32) {
+    for (int r = 0; r < rows; ++r) merge_row_warp<T>(p, u, r);
+    return;
+  }
+  const int per = max(1, 32 / cc);
+  for (int r0 = 0; r0 < rows; r0 += per) merge_chunk_warp<T>(p, u, r0, min(per, rows - r0));
+}
+
 template <typename T> struct HasTiles { static constexpr bool v = false; };
 template <> struct HasTiles<__nv_bfloat16> { static constexpr bool v = true; };
 template <> struct HasTiles<__half> { static constexpr bool v = true; };
@@ -519,8 +621,15 @@ __device__ __forceinline__ void cta_arrive_and_merge(const KParams& p, const Ite
       for (int i = 0; i < nm; ++i) {
         const int u = s_merge[i];
         const int rows = __ldg(p.units + (int64_t)u * kUnitWords + kUnRows);
-        for (int r = 0; r < rows; ++r, ++k)
-          if ((k & (kWarps - 1)) == warp) merge_row_warp<T>(p, u, r);
+        const int cc = __ldg(p.units + (int64_t)u * kUnitWords + kUnContribCount);
+        if (cc > 32) {
+          for (int r = 0; r < rows; ++r, ++k)
+            if ((k & (kWarps - 1)) == warp) merge_row_warp<T>(p, u, r);
+          continue;
+        }
+        const int per = max(1, 32 / cc);
+        for (int r0 = 0; r0 < rows; r0 += per, ++k)
+          if ((k & (kWarps - 1)) == warp) merge_chunk_warp<T>(p, u, r0, min(per, rows - r0));
       }
       return;
     }
@@ -549,9 +658,7 @@ __device__ __forceinline__ void warp_arrive_and_merge(const KParams& p, const It
   while (last) {
     const int bit = __ffs(last) - 1;
     last &= last - 1;
-    const int u = it.u0 + bit;
-    const int rows = __ldg(p.units + (int64_t)u * kUnitWords + kUnRows);
-    for (int r = 0; r < rows; ++r) merge_row_warp<T>(p, u, r);
+    merge_unit_warp<T>(p, it.u0 + bit);
   }
 }
 
@@ -568,6 +675,7 @@ __global__ void __launch_bounds__(kThreads, 2) psa_persistent(const __grid_const
   __shared__ tile::Barriers s_bar;
   __shared__ uint32_t s_tmem;
   __shared__ vec::Shared s_vec;
+  __shared__ dec::Shared s_dec;
   __shared__ A s_rowM[kTileM], s_rowL[kTileM];
   __shared__ A s_fac[kWarps * 8];
 
@@ -575,6 +683,8 @@ __global__ void __launch_bounds__(kThreads, 2) psa_persistent(const __grid_const
   const int64_t t_kernel0 = (p.trace_cap > 0 && threadIdx.x == 0) ? int64_t(globaltimer()) : 0;
   tile::State tst{0u, 0u, 0u};
   const bool tiles = kTiles && p.use_tiles;
+  const bool dec_on = kVecFast && p.use_dec;
+  const bool tmem_on = tiles || dec_on;
   if (kVecFast) {
     if (threadIdx.x == 0) vec::init_barriers(&s_vec);
     if (threadIdx.x == 32) {
@@ -585,8 +695,15 @@ __global__ void __launch_bounds__(kThreads, 2) psa_persistent(const __grid_const
     }
     __syncthreads();
   }
-  if (kTiles && !tiles && warp == 5) dev::tmem_relinquish();
-  if (tiles) {
+  if (kTiles && !tmem_on && warp == 5) dev::tmem_relinquish();
+  if (dec_on && threadIdx.x == 0) dec::init_barriers(&s_dec);
+  if (dec_on && threadIdx.x == 4 * 32) {
+    dev::tma_prefetch_desc(&p.tmd_kp);
+    dev::tma_prefetch_desc(&p.tmd_vp);
+    dev::tma_prefetch_desc(&p.tmd_kd);
+    dev::tma_prefetch_desc(&p.tmd_vd);
+  }
+  if (tmem_on) {
     if (threadIdx.x == 0) tile::init_barriers(&s_bar);
     if (warp == 4 && lane == 0) {
       dev::tma_prefetch_desc(&p.tm_q);
@@ -655,7 +772,60 @@ __global__ void __launch_bounds__(kThreads, 2) psa_persistent(const __grid_const
         if (p.trace_cap > 0 && lane == 0) trace_item(p, idx, it.kind, t0);
       }
     };
-    if (int(blockIdx.x) < p.n_tile_ctas) {
+    auto dec_phase = [&]() {
+      auto load_at = [&](int idx) { return load_item(p.items + (int64_t)idx * kItemWords); };
+      auto finish = [&](const ItemRec& it, int t, int R, const float (&m)[dec::kR],
+                        const float (&L)[dec::kR], const float (&ov)[dec::kR]) {
+        if (it.ws_row >= 0) {
+          float* wo = static_cast<float*>(p.ws_o);
+#pragma unroll
+          for (int r = 0; r < dec::kR; ++r)
+            if (r < R) wo[((int64_t)it.ws_row + r) * 128 + t] = ov[r];
+          if (t == 0) {
+#pragma unroll
+            for (int r = 0; r < dec::kR; ++r)
+              if (r < R)
+                *reinterpret_cast<float2*>(static_cast<float*>(p.ws_ml) + ((int64_t)it.ws_row + r) * 2) =
+                    make_float2(m[r], L[r]);
+          }
+          dec::named_sync_softmax();
+          if (t == 0) {
+            __threadfence();  // release: this item's partial rows
+            bool any = false;
+            for (int u = it.u0; u < it.u1; ++u) {
+              const int need = __ldg(p.units + (int64_t)u * kUnitWords + kUnContribCount);
+              if (atomicAdd(p.unit_cnt + u, 1) == need - 1) {
+                p.unit_cnt[u] = 0;
+                dec::enqueue_merge(&s_dec, u);
+                any = true;
+              }
+            }
+            (void)any;
+          }
+        } else {
+          const int64_t tok0 = __ldg(p.group_tok0 + it.g);
+#pragma unroll
+          for (int r = 0; r < dec::kR; ++r) {
+            if (r < R) {
+              const int row = it.row0 + r;
+              const int64_t idx = (tok0 + row / p.gqa) * p.Hq + (int64_t)it.h * p.gqa + row % p.gqa;
+              static_cast<T*>(p.out)[idx * 128 + t] = from_acc<T>(ov[r] / L[r]);
+              if (t == 0) {
+                if (!(L[r] > 0.f)) atomicOr(&p.ctrl->error, 1);
+                if (p.lse) p.lse[idx] = (m[r] + log2f(L[r])) * Dom<float>::kToNat;
+              }
+            }
+          }
+        }
+      };
+      auto merge_u = [&](int u) { merge_unit_warp<T>(p, u); };
+      dec::run<T>(p, smem, &s_dec, tst.tmem, load_at, finish, merge_u);
+    };
+    if (dec_on) {
+      cta_phase(p.n_tile_items);
+      __syncthreads();
+      dec_phase();
+    } else if (int(blockIdx.x) < p.n_tile_ctas) {
       cta_phase(p.n_tile_items);
       warp_phase();
     } else {
@@ -680,7 +850,7 @@ __global__ void __launch_bounds__(kThreads, 2) psa_persistent(const __grid_const
       __threadfence();
     }
   }
-  if (tiles) {
+  if (tmem_on) {
     dev::tc_fence_before();
     __syncthreads();
     if (warp == 5) dev::tmem_dealloc<tile::kTmemCols>(tst.tmem);
@@ -743,7 +913,7 @@ size_t smem_for(const KParams& p, int mode) {
     if (t > smem) smem = t;
   }
   if (HasTiles<T>::v && mode == kModeFast) {
-    const size_t v = vec::smem_bytes(p.d);
+    const size_t v = p.use_dec ? dec::smem_bytes() : vec::smem_bytes(p.d);
     if (v > smem) smem = v;
   }
   return smem;
@@ -834,6 +1004,10 @@ int encode_kv(CUtensorMap* m, CUtensorMapDataType dt, const void* base, int64_t 
 }
 }  // namespace
 
+bool dec_supported(int32_t dtype, int32_t d, int32_t dv) {
+  return (dtype == PSA_DTYPE_BF16 || dtype == PSA_DTYPE_F16) && d == 128 && dv == 128;
+}
+
 bool vec_fast_supported(int32_t dtype, int32_t d, int32_t dv) {
   return (dtype == PSA_DTYPE_BF16 || dtype == PSA_DTYPE_F16) && d == dv && (d == 64 || d == 128);
 }
@@ -860,6 +1034,12 @@ int encode_tile_maps(KParams& p, int32_t dtype, int64_t T, int64_t prefix_keys,
     if (!e) e = encode_kv(&p.tm_vp, dt, p.vp, prefix_keys, p.Hkv, p.dv, 64, tile::kBN, true);
     if (!e) e = encode_kv(&p.tm_kd, dt, p.kd, distinct_keys, p.Hkv, p.d, 64, tile::kBN, true);
     if (!e) e = encode_kv(&p.tm_vd, dt, p.vd, distinct_keys, p.Hkv, p.dv, 64, tile::kBN, true);
+  }
+  if (!e && p.use_dec) {
+    e = encode_kv(&p.tmd_kp, dt, p.kp, prefix_keys, p.Hkv, p.d, 64, dec::kBK, true);
+    if (!e) e = encode_kv(&p.tmd_vp, dt, p.vp, prefix_keys, p.Hkv, p.dv, 64, dec::kBK, true);
+    if (!e) e = encode_kv(&p.tmd_kd, dt, p.kd, distinct_keys, p.Hkv, p.d, 64, dec::kBK, true);
+    if (!e) e = encode_kv(&p.tmd_vd, dt, p.vd, distinct_keys, p.Hkv, p.dv, 64, dec::kBK, true);
   }
   if (!e && p.use_vec_fast) {
     e = encode_kv(&p.tmv_kp, dt, p.kp, prefix_keys, p.Hkv, p.d, p.d, vec::kKB, false);

@@ -31,6 +31,11 @@ struct KParams {
   alignas(64) CUtensorMap tmv_vp;
   alignas(64) CUtensorMap tmv_kd;
   alignas(64) CUtensorMap tmv_vd;
+  // tcgen05 decode path: k/v as 3-D (d, Hkv, keys), (64, 1, 128) boxes, 128-byte swizzle.
+  alignas(64) CUtensorMap tmd_kp;
+  alignas(64) CUtensorMap tmd_vp;
+  alignas(64) CUtensorMap tmd_kd;
+  alignas(64) CUtensorMap tmd_vd;
   const void* q;
   const void* kp;
   const void* vp;
@@ -58,6 +63,8 @@ struct KParams {
   int32_t use_tiles;     // the plan has TILE items: allocate TMEM, init barriers
   int32_t use_vec_fast;  // bf16/f16, d == dv in {64, 128}: TMA-staged decode path
   int32_t trace_cap;     // diagnostics: capacity (items) of `trace`, 0 = off
+  int32_t use_dec;       // VEC items on the tcgen05 decode pipeline (d == dv == 128)
+  int32_t pad2;
   double scale;
   int64_t* trace;        // diagnostics: per item {cta | smid << 32, kind, t_start, t_end}
 };
@@ -68,6 +75,8 @@ int encode_tile_maps(KParams& p, int32_t dtype, int64_t T, int64_t prefix_keys,
                      int64_t distinct_keys);
 // True when the VEC fast path applies to this dtype / head shape.
 bool vec_fast_supported(int32_t dtype, int32_t d, int32_t dv);
+// True when VEC items can run on the tcgen05 decode pipeline.
+bool dec_supported(int32_t dtype, int32_t d, int32_t dv);
 
 // Launches one persistent grid on `stream`. Returns a cudaError_t value.
 int launch_psa(const KParams& p, int32_t dtype, int32_t num_sms, int32_t ctas_per_sm,

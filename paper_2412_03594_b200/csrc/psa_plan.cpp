@@ -5,6 +5,7 @@
 #include <algorithm>
 #include <array>
 #include <numeric>
+#include <utility>
 
 #include "../../include/psa.h"
 
@@ -96,30 +97,50 @@ std::string build_plan(const PlanInput& in, const PlanOptions& opt, Plan* out) {
   //    item writes a 128-row fp32 partial, so fewer, longer tiles are cheaper.
   //    VEC items (warp-level) aim at kVecWaves waves over all warps, capped at
   //    kVecMaxKeys keys so a long segment spreads over many warps.
-  int64_t total_tile = 0, total_vec = 0;
+  int64_t total_vec = 0;
+  std::vector<std::pair<int64_t, int64_t>> tile_segs;  // (row blocks x Hkv, keys)
   for (int32_t g = 0; g < in.G; ++g) {
     const int64_t tok0 = in.cu_q[in.cu_req[g]];
     const int64_t Ng = gqa * (in.cu_q[in.cu_req[g + 1]] - tok0);
     const int64_t P = in.cu_prefix[g + 1] - in.cu_prefix[g];
     if (P > 0) {
       const int32_t k = kind_for(Ng);
-      (k == kItemTile ? total_tile : total_vec) += ceil_div(Ng, step_for(k)) * P;
+      const int64_t blocks = ceil_div(Ng, step_for(k));
+      if (k == kItemTile) tile_segs.emplace_back(blocks * in.Hkv, P);
+      else total_vec += blocks * P;
     }
     for (int64_t r = in.cu_req[g]; r < in.cu_req[g + 1]; ++r) {
       const int64_t D = in.cu_distinct[r + 1] - in.cu_distinct[r];
       const int64_t nr = gqa * (in.cu_q[r + 1] - in.cu_q[r]);
       if (D > 0) {
         const int32_t k = kind_for(nr);
-        (k == kItemTile ? total_tile : total_vec) += ceil_div(nr, step_for(k)) * D;
+        const int64_t blocks = ceil_div(nr, step_for(k));
+        if (k == kItemTile) tile_segs.emplace_back(blocks * in.Hkv, D);
+        else total_vec += blocks * D;
       }
     }
   }
-  total_tile *= in.Hkv;
   total_vec *= in.Hkv;
   const int64_t ctas = int64_t(std::max(1, opt.num_sms)) * std::max(1, opt.ctas_per_sm);
-  int64_t chunk = ceil_div(total_tile, ctas * std::max(1, opt.target_waves));
-  chunk = std::min<int64_t>(std::max<int64_t>(chunk, opt.min_chunk_keys), opt.max_chunk_keys);
-  chunk = round_up(std::max<int64_t>(chunk, 1), kChunkAlign);
+  // Tile chunk: the smallest multiple of kChunkAlign in [min, max] whose item count
+  // fits target_waves waves of CTAs (binary search; item count is monotone).
+  const int64_t tile_target = ctas * std::max(1, opt.target_waves);
+  auto tile_items = [&](int64_t ck) {
+    int64_t n = 0;
+    for (const auto& sg : tile_segs) n += sg.first * ceil_div(sg.second, ck);
+    return n;
+  };
+  int64_t lo = round_up(std::max<int64_t>(opt.min_chunk_keys, 1), kChunkAlign);
+  int64_t hi = std::max(lo, round_up(std::max<int64_t>(opt.max_chunk_keys, 1), kChunkAlign));
+  if (tile_items(lo) > tile_target) {
+    while (lo < hi) {
+      const int64_t mid = round_up((lo + hi) / 2, kChunkAlign);
+      if (mid >= hi) break;
+      if (tile_items(mid) <= tile_target) hi = mid; else lo = mid + kChunkAlign;
+    }
+    lo = tile_items(lo) <= tile_target ? lo : hi;
+  }
+  const int64_t chunk = lo;
   int64_t vchunk = ceil_div(total_vec, ctas * kVecWarps * kVecWaves);
   vchunk = std::min<int64_t>(std::max<int64_t>(vchunk, kChunkAlign), kVecMaxKeys);
   vchunk = round_up(vchunk, kChunkAlign);

@@ -13,8 +13,8 @@
 //              two independent 2-stage rings
 //   warp 5     MMA issuer (one lane): S = Q K^T (A, B from smem) and
 //              O += P V (A = P from TMEM, B = V from smem) with tcgen05.mma
-// TMEM (256 columns per CTA, 2 CTAs/SM): S [0, 64), P (bf16 pairs) [64, 96),
-// O [128, 128+dv). Shared memory (d = dv = 128): Q 32 KB, K 2 x 16 KB,
+// TMEM (256 columns per CTA, 2 CTAs/SM): S [0, 64), P (bf16 pairs) double-buffered
+// [64, 96) / [96, 128), O [128, 128+dv). Shared memory (d = dv = 128): Q 32 KB, K 2 x 16 KB,
 // V 2 x 16 KB.
 //
 // Pipelining: a K stage is released as soon as S_j = Q K_j^T has completed and
@@ -37,7 +37,7 @@ constexpr int kM = 128;          // rows per tile (UMMA M)
 constexpr int kStages = 2;
 constexpr uint32_t kTmemCols = 256;
 constexpr uint32_t kTmemS = 0;
-constexpr uint32_t kTmemP = 64;
+constexpr uint32_t kTmemP = 64;   // two P buffers: [64, 96) and [96, 128)
 constexpr uint32_t kTmemO = 128;
 constexpr float kRescaleThreshold = 8.0f;  // log2 units
 
@@ -50,7 +50,7 @@ struct Barriers {
   uint64_t s_full;
   uint64_t s_free;
   uint64_t p_full[kStages];  // per stage so a fast softmax can never lap the MMA waiter
-  uint64_t o_done;
+  uint64_t o_done[2];        // PV_n completes phase n >> 1 of o_done[n & 1]
 };
 
 // Running phase bookkeeping, identical in every thread of the CTA.
@@ -76,7 +76,8 @@ __device__ __forceinline__ void init_barriers(Barriers* b) {
   }
   dev::mbar_init(&b->s_full, 1);
   dev::mbar_init(&b->s_free, 4);
-  dev::mbar_init(&b->o_done, 1);
+  dev::mbar_init(&b->o_done[0], 1);
+  dev::mbar_init(&b->o_done[1], 1);
   dev::fence_mbar_init();
 }
 
@@ -247,10 +248,10 @@ __device__ __forceinline__ State tile_item(const KParams& p, const ItemT& it, ui
         dbg_event(p, st, kEvPvIssue, jb);
         for (int kk = 0; kk < kBN / 16; ++kk) {
           const uint64_t b = dev::umma_desc_sw128(v_addr + kk * (16 * 128), kBN * 128, 1024);
-          dev::mma_f16_ts(tO, tP + kk * 8, b, idesc_o, (jb > 0 || kk > 0));
+          dev::mma_f16_ts(tO, tP + s * 32 + kk * 8, b, idesc_o, (jb > 0 || kk > 0));
         }
         dev::mma_commit(&bar->v_empty[s]);
-        dev::mma_commit(&bar->o_done);
+        dev::mma_commit(&bar->o_done[n & 1]);
       }
     }
   } else if (warp < 4) {
@@ -294,36 +295,41 @@ __device__ __forceinline__ State tile_item(const KParams& p, const ItemT& it, ui
       if (m == -INFINITY) {
         m = mb;
       } else if (mb > m + kRescaleThreshold) {
-        alpha = exp2f(m - mb);
+        alpha = dev::ex2(m - mb);
         m = mb;
         rescale = true;
       }
       l *= alpha;
       // P_n (bf16 pairs) replaces S_n's registers in place: r0[i] = pack(p_2i, p_2i+1).
       const float nm = -m;
+      float l4[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
       for (int i = 0; i < 16; ++i) {
-        const float e0 = exp2f(fmaf(__uint_as_float(r0[2 * i]), sc, nm));
-        const float e1 = exp2f(fmaf(__uint_as_float(r0[2 * i + 1]), sc, nm));
-        l += e0 + e1;
+        const float e0 = dev::ex2(fmaf(__uint_as_float(r0[2 * i]), sc, nm));
+        const float e1 = dev::ex2(fmaf(__uint_as_float(r0[2 * i + 1]), sc, nm));
+        l4[i & 3] += e0 + e1;
         r0[i] = pack2<T>(e0, e1);
       }
 #pragma unroll
       for (int i = 0; i < 16; ++i) {
-        const float e0 = exp2f(fmaf(__uint_as_float(r1[2 * i]), sc, nm));
-        const float e1 = exp2f(fmaf(__uint_as_float(r1[2 * i + 1]), sc, nm));
-        l += e0 + e1;
+        const float e0 = dev::ex2(fmaf(__uint_as_float(r1[2 * i]), sc, nm));
+        const float e1 = dev::ex2(fmaf(__uint_as_float(r1[2 * i + 1]), sc, nm));
+        l4[i & 3] += e0 + e1;
         r0[16 + i] = pack2<T>(e0, e1);
       }
-      // P TMEM and O are read by PV_{n-1}: it must be complete before we overwrite
-      // P or rescale O.
-      if (jb > 0) {
-        dev::mbar_wait(&bar->o_done, (n - 1) & 1);
+      l += (l4[0] + l4[1]) + (l4[2] + l4[3]);
+      // P is double-buffered in TMEM (P_n in buffer n & 1): PV_{n-2} finished with it
+      // before S_n could be computed... except across the wait below, which also
+      // orders the rare O rescale after PV_{n-1}.
+      if (jb > 1) {
+        dev::mbar_wait(&bar->o_done[n & 1], ((n - 2) >> 1) & 1);
         dev::tc_fence_after();
       }
-      dev::tmem_st32(tP, r0);
+      dev::tmem_st32(tP + s * 32, r0);
       if (__any_sync(0xffffffffu, rescale)) {
         // O holds PV_0..PV_{n-1}: scale rows in place before PV_n accumulates.
+        dev::mbar_wait(&bar->o_done[(n - 1) & 1], ((n - 1) >> 1) & 1);
+        dev::tc_fence_after();
         for (int c = 0; c < dv; c += 32) {
           uint32_t o[32];
           dev::tmem_ld32(tO + c, o);
@@ -341,7 +347,10 @@ __device__ __forceinline__ State tile_item(const KParams& p, const ItemT& it, ui
     }
     if (threadIdx.x == 0) dbg_event(p, st, kEvMisc, 0);
     // ---------------- epilogue ----------------
-    dev::mbar_wait(&bar->o_done, (base_blk + nb - 1) & 1);
+    {
+      const uint32_t last = base_blk + nb - 1;
+      dev::mbar_wait(&bar->o_done[last & 1], (last >> 1) & 1);
+    }
     dev::tc_fence_after();
     const bool valid = row < it.nrows;
     if (it.ws_row >= 0) {

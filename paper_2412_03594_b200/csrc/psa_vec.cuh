@@ -45,9 +45,9 @@ __host__ __device__ constexpr size_t smem_bytes(int d) {
   return size_t(kWarps) * kStages * 2 * kKB * d * 2 + 128;
 }
 
-struct Shared {
+struct alignas(16) Shared {
   uint64_t full[kWarps][kStages];
-  float p[kWarps][32];
+  alignas(16) float p[kWarps][32];  // read back as float4
 };
 
 __device__ __forceinline__ void init_barriers(Shared* s) {
@@ -169,10 +169,10 @@ __device__ __forceinline__ uint32_t warp_item(const KParams& p, const ItemT& it,
       bm = fmaxf(bm, __shfl_xor_sync(0xffffffffu, bm, 16));
       float alpha = 1.f;
       if (bm > m + kRescaleThreshold) {  // also the first block (m = -inf)
-        alpha = exp2f(m - bm);
+        alpha = dev::ex2(m - bm);
         m = bm;
       }
-      const float pe = exp2f(x - m);
+      const float pe = dev::ex2(x - m);
       lp = lp * alpha + pe;
       if (__any_sync(0xffffffffu, alpha != 1.f)) {
 #pragma unroll

@@ -47,8 +47,8 @@ def _device_batch(a, dtype):
 
 @pytest.mark.parametrize("spec", _manifest(), ids=lambda s: s["name"])
 @pytest.mark.parametrize("opts", [dict(), dict(disable_tiles=1), dict(min_chunk_keys=64),
-                                  dict(disable_vec_fast=1)],
-                         ids=["default", "no_tiles", "small_chunks", "generic_vec"])
+                                  dict(disable_vec_fast=1), dict(disable_vec_fast=2)],
+                         ids=["default", "no_tiles", "small_chunks", "generic_vec", "warp_vec"])
 def test_packed_matches_reference_golden(spec, opts):
     a = C.make_packed(spec)
     want = np.load(os.path.join(GOLDEN, "packed.npz"))[spec["name"]]
