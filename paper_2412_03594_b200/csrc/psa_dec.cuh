@@ -47,7 +47,7 @@ struct alignas(16) Shared {
   float red[4][kR];   // per-warp partial row maxima / sums
   // merge queue: softmax thread 0 appends the units this CTA completes, warps 6-7 merge them
   int mq[64];
-  int mq_tail, mq_head, mq_done, mq_closed;
+  int mq_tail, mq_head, mq_done, mq_closed, mq_resv;
 };
 
 __device__ __forceinline__ void init_barriers(Shared* s) {
@@ -65,20 +65,22 @@ __device__ __forceinline__ void init_barriers(Shared* s) {
   dev::mbar_init(&s->s_full, 1);
   dev::mbar_init(&s->s_free, 4);
   dev::mbar_init(&s->o_done, 1);
-  s->mq_tail = s->mq_head = s->mq_done = s->mq_closed = 0;
+  s->mq_tail = s->mq_head = s->mq_done = s->mq_closed = s->mq_resv = 0;
   dev::fence_mbar_init();
 }
 
 __device__ __forceinline__ int ld_volatile(const int* p) { return *reinterpret_cast<const volatile int*>(p); }
 __device__ __forceinline__ void st_volatile(int* p, int v) { *reinterpret_cast<volatile int*>(p) = v; }
 
-// Softmax thread 0: hand unit u to the merge warps (bounded ring, spins only if 64 are pending).
+// Softmax threads: hand unit u to the merge warps (bounded ring; spins only if 64 are pending).
+// Slots are reserved with an atomic and published in order through mq_tail.
 __device__ __forceinline__ void enqueue_merge(Shared* sh, int u) {
-  const int tail = sh->mq_tail;
-  while (tail - ld_volatile(&sh->mq_done) >= 64) __nanosleep(64);
-  st_volatile(&sh->mq[tail & 63], u);
+  const int slot = atomicAdd(&sh->mq_resv, 1);
+  while (slot - ld_volatile(&sh->mq_done) >= 64) __nanosleep(64);
+  st_volatile(&sh->mq[slot & 63], u);
   __threadfence_block();
-  st_volatile(&sh->mq_tail, tail + 1);
+  while (ld_volatile(&sh->mq_tail) != slot) __nanosleep(32);  // publish in slot order
+  st_volatile(&sh->mq_tail, slot + 1);
 }
 
 // Warps 6-7: merge queued units until the queue is closed and drained.

@@ -594,23 +594,23 @@ template <typename T, typename A>
 __device__ __forceinline__ void cta_arrive_and_merge(const KParams& p, const ItemRec& it,
                                                      int* s_merge, int* s_nmerge, A* s_rowM,
                                                      A* s_rowL) {
-  // Publish this item's partial rows: CTA barrier, then one gpu-scope fence by the
-  // thread that signals (release is cumulative over the barrier).
+  // Publish this item's partial rows: CTA barrier, then the arrivals — one thread per
+  // unit, in parallel (a serial loop of returning atomics costs one L2 round trip
+  // per unit), each after a gpu-scope fence (release is cumulative over the barrier).
+  if (threadIdx.x == 0) *s_nmerge = 0;
   __syncthreads();
-  if (threadIdx.x == 0) {
+  const int nu = it.u1 - it.u0;
+  for (int i = threadIdx.x; i < nu; i += kThreads) {
+    const int u = it.u0 + i;
     __threadfence();
-    int n = 0;
-    for (int u = it.u0; u < it.u1; ++u) {
-      const int need = __ldg(p.units + (int64_t)u * kUnitWords + kUnContribCount);
-      const int old = atomicAdd(p.unit_cnt + u, 1);
-      if (old == need - 1) {
-        s_merge[n++] = u;
-        p.unit_cnt[u] = 0;  // every contribution has arrived: reset for the next launch
-      }
+    const int need = __ldg(p.units + (int64_t)u * kUnitWords + kUnContribCount);
+    if (atomicAdd(p.unit_cnt + u, 1) == need - 1) {
+      p.unit_cnt[u] = 0;  // every contribution has arrived: reset for the next launch
+      s_merge[atomicAdd(s_nmerge, 1)] = u;
     }
-    *s_nmerge = n;
-    if (n) __threadfence();  // acquire side for the partials about to be read
   }
+  __syncthreads();
+  if (threadIdx.x == 0 && *s_nmerge) __threadfence();  // acquire side for the partials
   __syncthreads();
   const int nm = *s_nmerge;
   if (!nm) return;
@@ -643,18 +643,18 @@ __device__ __forceinline__ void warp_arrive_and_merge(const KParams& p, const It
   const int lane = threadIdx.x & 31;
   __threadfence();  // one warp-wide fence: publishes every lane's partial rows
   __syncwarp();
-  uint32_t last = 0;
-  if (lane == 0) {
-    for (int u = it.u0; u < it.u1 && u - it.u0 < 32; ++u) {
-      const int need = __ldg(p.units + (int64_t)u * kUnitWords + kUnContribCount);
-      if (atomicAdd(p.unit_cnt + u, 1) == need - 1) {
-        last |= 1u << (u - it.u0);
-        p.unit_cnt[u] = 0;
-      }
+  // one lane per unit (items of <= 8 rows cover <= 9 units)
+  bool is_last = false;
+  const int u = it.u0 + lane;
+  if (u < it.u1) {
+    const int need = __ldg(p.units + (int64_t)u * kUnitWords + kUnContribCount);
+    if (atomicAdd(p.unit_cnt + u, 1) == need - 1) {
+      p.unit_cnt[u] = 0;
+      is_last = true;
     }
-    if (last) __threadfence();
   }
-  last = __shfl_sync(0xffffffffu, last, 0);
+  uint32_t last = __ballot_sync(0xffffffffu, is_last);
+  if (last) __threadfence();
   while (last) {
     const int bit = __ffs(last) - 1;
     last &= last - 1;
@@ -789,18 +789,15 @@ __global__ void __launch_bounds__(kThreads, 2) psa_persistent(const __grid_const
                     make_float2(m[r], L[r]);
           }
           dec::named_sync_softmax();
-          if (t == 0) {
-            __threadfence();  // release: this item's partial rows
-            bool any = false;
-            for (int u = it.u0; u < it.u1; ++u) {
-              const int need = __ldg(p.units + (int64_t)u * kUnitWords + kUnContribCount);
-              if (atomicAdd(p.unit_cnt + u, 1) == need - 1) {
-                p.unit_cnt[u] = 0;
-                dec::enqueue_merge(&s_dec, u);
-                any = true;
-              }
+          const int nu = it.u1 - it.u0;  // <= 9 units: one thread each
+          if (t < nu) {
+            const int u = it.u0 + t;
+            __threadfence();  // release: this item's partial rows (cumulative over the barrier)
+            const int need = __ldg(p.units + (int64_t)u * kUnitWords + kUnContribCount);
+            if (atomicAdd(p.unit_cnt + u, 1) == need - 1) {
+              p.unit_cnt[u] = 0;
+              dec::enqueue_merge(&s_dec, u);
             }
-            (void)any;
           }
         } else {
           const int64_t tok0 = __ldg(p.group_tok0 + it.g);

@@ -60,14 +60,24 @@ def report(tr: np.ndarray, tables: dict) -> dict:
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--config", default="c2")
+    ap.add_argument("--ctas-per-sm", type=int, default=0)
+    ap.add_argument("--min-chunk", type=int, default=0)
+    ap.add_argument("--waves", type=int, default=0)
+    ap.add_argument("--groups", type=int, default=0)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--json")
     args = ap.parse_args()
     dev = torch.device("cuda", 0)
     spec = W.config(args.config)
+    if args.groups:
+        spec = spec.subset([g % spec.G for g in range(args.groups)])
+        spec.group_ids = list(range(args.groups))
     b = W.make_batch(spec, dev)
     op = P.PrefixSharedAttention(b["cu_req"], b["cu_q"], b["cu_prefix"], b["cu_distinct"],
-                                 spec.Hq, spec.Hkv, spec.d, spec.dv, spec.torch_dtype, dev)
+                                 spec.Hq, spec.Hkv, spec.d, spec.dv, spec.torch_dtype, dev,
+                                 options=P.PlanOptions(ctas_per_sm=args.ctas_per_sm,
+                                                       min_chunk_keys=args.min_chunk,
+                                                       target_waves=args.waves))
     inputs = (b["q"], b["k_prefix"], b["v_prefix"], b["k_distinct"], b["v_distinct"])
     for _ in range(args.warmup):
         op(*inputs)
