@@ -28,30 +28,30 @@ namespace dec {
 constexpr int kBK = 128;               // keys per block (MMA M)
 constexpr int kN = 16;                 // query rows per item (MMA N), padded
 constexpr int kR = 8;                  // rows per VEC item (planner kVecRows)
-constexpr int kSlots = 3;              // K/V ring slots
+constexpr int kMaxSlots = 6;           // K/V ring slots: p.dec_slots (3 with 2 CTAs/SM, 6 with 1)
 constexpr int kSlotBytes = kBK * 128 * 2;  // one K or V block, d = 128 bf16 = 32 KB
 constexpr int kQBytes = kN * 128 * 2;  // one item's Q rows = 4 KB
 constexpr int kPBytes = kN * kBK * 2;  // P^T = 4 KB
 constexpr uint32_t kTmemS = 0, kTmemO = 32;
 constexpr float kRescaleThreshold = 8.0f;
 
-__host__ __device__ constexpr size_t smem_bytes() {
-  return size_t(kSlots) * kSlotBytes + 2 * kQBytes + kPBytes + 1024;
+__host__ __device__ constexpr size_t smem_bytes(int slots) {
+  return size_t(slots) * kSlotBytes + 2 * kQBytes + kPBytes + 1024;
 }
 
 struct alignas(16) Shared {
-  uint64_t slot_full[kSlots], slot_empty[kSlots];
+  uint64_t slot_full[kMaxSlots], slot_empty[kMaxSlots];
   uint64_t item_full[2], item_empty[2];
   uint64_t s_full, s_free, p_full[2], o_done, o_full[2], o_empty[2];
   int item_idx[2];
-  float red[4][kR];   // per-warp partial row maxima / sums
+  float red[2][4][kR];  // per-warp partial row maxima (double-buffered by block parity) / sums
   // merge queue: softmax thread 0 appends the units this CTA completes, warps 6-7 merge them
   int mq[64];
   int mq_tail, mq_head, mq_done, mq_closed, mq_resv;
 };
 
 __device__ __forceinline__ void init_barriers(Shared* s) {
-  for (int i = 0; i < kSlots; ++i) {
+  for (int i = 0; i < kMaxSlots; ++i) {
     dev::mbar_init(&s->slot_full[i], 1);
     dev::mbar_init(&s->slot_empty[i], 1);
   }
@@ -106,21 +106,33 @@ __device__ __forceinline__ void merge_loop(Shared* sh, MergeUnit&& merge_unit) {
   }
 }
 
+// Diagnostics: clock64 of per-block events of CTA 0's first 64 decode blocks, after
+// the tile events (psa_debug_set_trace). Slot = (16 + event) * 64 + global block.
+__device__ __forceinline__ void dbg(const KParams& p, int ev, uint32_t g) {
+  if (p.trace_cap > 0 && blockIdx.x == 0 && g < 64) {
+    long long t;
+    asm volatile("mov.u64 %0, %%clock64;" : "=l"(t));
+    p.trace[(int64_t(p.num_items) + 4096) * 4 + (16 + ev) * 64 + g] = t;
+  }
+}
+
 __device__ __forceinline__ void named_sync_softmax() {  // warps 0-3
   asm volatile("bar.sync 1, 128;" ::: "memory");
 }
 
 struct Geo {
   uint8_t* base;  // 1024-aligned
+  uint32_t slots;
   __device__ __forceinline__ uint8_t* slot(uint32_t i) const { return base + i * kSlotBytes; }
   __device__ __forceinline__ uint8_t* q(uint32_t i) const {
-    return base + kSlots * kSlotBytes + i * kQBytes;
+    return base + slots * kSlotBytes + i * kQBytes;
   }
-  __device__ __forceinline__ uint8_t* pt() const { return base + kSlots * kSlotBytes + 2 * kQBytes; }
+  __device__ __forceinline__ uint8_t* pt() const { return base + slots * kSlotBytes + 2 * kQBytes; }
 };
 
-__device__ __forceinline__ Geo carve(uint8_t* smem_raw) {
+__device__ __forceinline__ Geo carve(uint8_t* smem_raw, int slots) {
   Geo g;
+  g.slots = uint32_t(slots);
   g.base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                       ~uintptr_t(1023));
   return g;
@@ -154,7 +166,8 @@ template <typename T, typename LoadItem, typename Finish, typename MergeUnit>
 __device__ void run(const KParams& p, uint8_t* smem_raw, Shared* sh, uint32_t tmem,
                     LoadItem&& load_item_at, Finish&& finish, MergeUnit&& merge_unit) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const Geo G = carve(smem_raw);
+  const Geo G = carve(smem_raw, p.dec_slots);
+  const uint32_t NSL = uint32_t(p.dec_slots);
   const int n_items = p.num_items;
 
   if (warp == 4) {
@@ -204,8 +217,9 @@ __device__ void run(const KParams& p, uint8_t* smem_raw, Shared* sh, uint32_t tm
           if (j < nbA) { km = &p.tmd_kp; vm = &p.tmd_vp; key = int(pbase + j * kBK); }
           else { km = &p.tmd_kd; vm = &p.tmd_vd; key = int(dbase + (j - nbA) * kBK); }
           for (int w = 0; w < 2; ++w, ++c) {  // K then V
-            const uint32_t s = c % kSlots;
-            dev::mbar_wait(&sh->slot_empty[s], ((c / kSlots) & 1) ^ 1);
+            const uint32_t s = c % NSL;
+            dev::mbar_wait(&sh->slot_empty[s], ((c / NSL) & 1) ^ 1);
+            dbg(p, w, c >> 1);
             dev::mbar_arrive_expect_tx(&sh->slot_full[s], kSlotBytes);
             const CUtensorMap* m = w == 0 ? km : vm;
             dev::tma_load_3d(G.slot(s), m, &sh->slot_full[s], 0, it.h, key);
@@ -250,10 +264,11 @@ __device__ void run(const KParams& p, uint8_t* smem_raw, Shared* sh, uint32_t tm
             progress = true;
           }
           if (nb_s > 0) {
-            const uint32_t cK = 2 * gS, s = cK % kSlots;
+            const uint32_t cK = 2 * gS, s = cK % NSL;
             const bool sfree = gS == 0 || dev::mbar_test(&sh->s_free, (gS - 1) & 1);
-            if (sfree && dev::mbar_test(&sh->slot_full[s], (cK / kSlots) & 1)) {
+            if (sfree && dev::mbar_test(&sh->slot_full[s], (cK / NSL) & 1)) {
               dev::tc_fence_after();
+              dbg(p, 2, gS);
               const uint32_t a0 = dev::smem_u32(G.slot(s)), b0 = dev::smem_u32(G.q(q));
               for (int kk = 0; kk < 8; ++kk) {
                 const uint32_t ch = kk >> 2, w = (kk & 3) * 32;
@@ -277,12 +292,13 @@ __device__ void run(const KParams& p, uint8_t* smem_raw, Shared* sh, uint32_t tm
         if (gP < gS) {
           const uint32_t q = k_p & 1, b = k_p & 1;
           if (nb_p < 0) { nb_p = nbs_ring[q]; j_p = 0; }
-          const uint32_t cV = 2 * gP + 1, s = cV % kSlots;
+          const uint32_t cV = 2 * gP + 1, s = cV % NSL;
           const bool need_o = j_p == 0;
           if (dev::mbar_test(&sh->p_full[gP & 1], (gP >> 1) & 1) &&
-              dev::mbar_test(&sh->slot_full[s], (cV / kSlots) & 1) &&
+              dev::mbar_test(&sh->slot_full[s], (cV / NSL) & 1) &&
               (!need_o || dev::mbar_test(&sh->o_empty[b], ((k_p >> 1) & 1) ^ 1))) {
             dev::tc_fence_after();
+            dbg(p, 3, gP);
             const uint32_t a0 = dev::smem_u32(G.slot(s));
             const uint32_t tO = tmem + kTmemO + b * kN;
             for (int kk = 0; kk < kBK / 16; ++kk) {
@@ -333,61 +349,72 @@ __device__ void run(const KParams& p, uint8_t* smem_raw, Shared* sh, uint32_t tm
       int64_t pbase, dbase;
       item_blocks(p, it, nbA, nb, pbase, dbase);
       const int R = it.nrows;
+      // rows >= R keep m = 0 and x = -inf: their exps are exactly 0, no NaN, and
+      // every row's arithmetic stays branch-free (the rows interleave for ILP).
       float m[kR], lp[kR];
 #pragma unroll
-      for (int r = 0; r < kR; ++r) { m[r] = -INFINITY; lp[r] = 0.f; }
+      for (int r = 0; r < kR; ++r) { m[r] = r < R ? -INFINITY : 0.f; lp[r] = 0.f; }
       for (int j = 0; j < nb; ++j, ++g) {
         const int nvalid = block_nvalid(it, nbA, j);
         dev::mbar_wait(&sh->s_full, g & 1);
+        if (t == 0) dbg(p, 4, g);
         dev::tc_fence_after();
         uint32_t sr[kN];
         dev::tmem_ld16(tS, sr);
         dev::tmem_wait_ld();
+        if (t == 0) dbg(p, 10, g);
         dev::tc_fence_before();
         __syncwarp();
         if (lane == 0) dev::mbar_arrive(&sh->s_free);
         const bool valid = t < nvalid;
         // block max per row: warp reduce, then across the 4 softmax warps
-        float x[kR];
+        float x[kR], v[kR];
 #pragma unroll
         for (int r = 0; r < kR; ++r) {
           x[r] = (valid && r < R) ? __uint_as_float(sr[r]) * sc : -INFINITY;
-          float v = x[r];
-          if (r < R) {
-#pragma unroll
-            for (int o = 16; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
-            if (lane == 0) sh->red[warp][r] = v;
-          }
+          v[r] = x[r];
         }
-        named_sync_softmax();
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1)
+#pragma unroll
+          for (int r = 0; r < kR; ++r) v[r] = fmaxf(v[r], __shfl_xor_sync(0xffffffffu, v[r], o));
+        if (lane == 0) {
+#pragma unroll
+          for (int r = 0; r < kR; ++r) sh->red[g & 1][warp][r] = v[r];
+        }
+        if (t == 0) dbg(p, 11, g);
+        named_sync_softmax();  // red[g & 1] is rewritten two blocks later, after another barrier
+        if (t == 0) dbg(p, 12, g);
+        const float (&rd)[4][kR] = sh->red[g & 1];
         float alpha[kR];
         bool any_rescale = false;
 #pragma unroll
         for (int r = 0; r < kR; ++r) {
-          alpha[r] = 1.f;
-          if (r < R) {
-            const float bm = fmaxf(fmaxf(sh->red[0][r], sh->red[1][r]),
-                                   fmaxf(sh->red[2][r], sh->red[3][r]));
-            if (bm > m[r] + kRescaleThreshold) {  // first block too (m = -inf)
-              alpha[r] = dev::ex2(m[r] - bm);
-              any_rescale |= (m[r] != -INFINITY);
-              m[r] = bm;
-            }
-          }
+          const float bm = fmaxf(fmaxf(rd[0][r], rd[1][r]), fmaxf(rd[2][r], rd[3][r]));
+          const bool up = bm > m[r] + kRescaleThreshold;  // also the first block (m = -inf)
+          alpha[r] = up ? dev::ex2(m[r] - bm) : 1.f;
+          any_rescale |= up && (m[r] != -INFINITY);
+          m[r] = up ? bm : m[r];
         }
-        named_sync_softmax();  // red[] may be rewritten by the next block only after all read it
-        // P^T (single buffer): PV_{g-1} must be done reading it (and O before rescale)
+        float e[kR];
+#pragma unroll
+        for (int r = 0; r < kR; ++r) {
+          e[r] = dev::ex2(x[r] - m[r]);
+          lp[r] = lp[r] * alpha[r] + e[r];
+        }
+        // P^T (single buffer): PV_{g-1} must be done reading it (and O before rescale);
+        // it was issued a whole softmax ago, so this wait rarely blocks.
+        if (t == 0) dbg(p, 13, g);
         if (g > 0) {
           dev::mbar_wait(&sh->o_done, (g - 1) & 1);
           dev::tc_fence_after();
         }
+        if (t == 0) dbg(p, 14, g);
 #pragma unroll
         for (int r = 0; r < kR; ++r) {
           if (r < R) {
-            const float e = dev::ex2(x[r] - m[r]);
-            lp[r] = lp[r] * alpha[r] + e;
             T h;
-            if constexpr (sizeof(T) == 2) h = T(e);
+            if constexpr (sizeof(T) == 2) h = T(e[r]);
             *reinterpret_cast<T*>(pt + sw128_off(r, t, kN)) = h;
           }
         }
@@ -402,27 +429,39 @@ __device__ void run(const KParams& p, uint8_t* smem_raw, Shared* sh, uint32_t tm
           dev::tmem_st16(tO, o);
           dev::tmem_wait_st();
         }
+        if (t == 0) dbg(p, 15, g);
         dev::fence_proxy_async_smem();
+        if (t == 0) dbg(p, 16, g);
         dev::tc_fence_before();
         __syncwarp();
         if (lane == 0) dev::mbar_arrive(&sh->p_full[g & 1]);
+        if (t == 0) dbg(p, 5, g);
       }
       // ---- item end: l per row, then O^T lane t = value column t
+      {
+        float v[kR];
 #pragma unroll
-      for (int r = 0; r < kR; ++r) {
-        if (r < R) {
-          float v = lp[r];
+        for (int r = 0; r < kR; ++r) v[r] = lp[r];
 #pragma unroll
-          for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-          if (lane == 0) sh->red[warp][r] = v;
+        for (int o = 16; o > 0; o >>= 1)
+#pragma unroll
+          for (int r = 0; r < kR; ++r) v[r] += __shfl_xor_sync(0xffffffffu, v[r], o);
+        if (lane == 0) {
+#pragma unroll
+          for (int r = 0; r < kR; ++r) sh->red[g & 1][warp][r] = v[r];
         }
       }
       named_sync_softmax();
       float L[kR];
+      {
+        const float (&rd)[4][kR] = sh->red[g & 1];
 #pragma unroll
-      for (int r = 0; r < kR; ++r)
-        L[r] = r < R ? (sh->red[0][r] + sh->red[1][r]) + (sh->red[2][r] + sh->red[3][r]) : 0.f;
+        for (int r = 0; r < kR; ++r)
+          L[r] = r < R ? (rd[0][r] + rd[1][r]) + (rd[2][r] + rd[3][r]) : 0.f;
+      }
+      if (t == 0) dbg(p, 7, g - 1);
       dev::mbar_wait(&sh->o_full[b], (k >> 1) & 1);
+      if (t == 0) dbg(p, 8, g - 1);
       dev::tc_fence_after();
       uint32_t o[kN];
       dev::tmem_ld16(tmem + kTmemO + b * kN + lane_base, o);
@@ -434,8 +473,10 @@ __device__ void run(const KParams& p, uint8_t* smem_raw, Shared* sh, uint32_t tm
 #pragma unroll
       for (int r = 0; r < kR; ++r) ov[r] = __uint_as_float(o[r]);
       finish(it, t, R, m, L, ov);  // writes output / partial, arrives at merge units
+      if (t == 0) dbg(p, 9, g - 1);
       named_sync_softmax();        // red[] reuse + item slot release after everyone finished
       if (t == 0) dev::mbar_arrive(&sh->item_empty[q]);
+      if (t == 0) dbg(p, 6, g - 1);
       if (p.trace_cap > 0 && t == 0 && idx < p.trace_cap) {
         long long t1;
         asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1));

@@ -900,25 +900,39 @@ __global__ void nonfinite_kernel(const T* x, int64_t n, int32_t* count) {
   if ((threadIdx.x & 31) == 0 && local) atomicAdd(count, local);
 }
 
+// Dynamic shared memory per CTA and the ring depths that fit it: 2 CTAs/SM get
+// ~110 KB each (tile: 2 K/V stages, decode: 3 slots), 1 CTA/SM gets ~220 KB
+// (tile: 4 stages, decode: 6 slots).
 template <typename T>
-size_t smem_for(const KParams& p, int mode) {
+size_t smem_for(KParams& p, int mode, int ctas_per_sm) {
   using A = typename AccOf<T>::type;
   constexpr int RP = sizeof(A) == 8 ? 2 : 4;
+  const size_t budget = (ctas_per_sm >= 2 ? size_t(227) * 1024 / 2 : size_t(227) * 1024) - 6 * 1024;
   size_t smem = mode == kModeFast ? 0 : size_t(kWarps) * RP * (p.dv + 2) * sizeof(A);
+  p.tile_stages = 2;
+  p.dec_slots = 3;
   if (HasTiles<T>::v && mode != kModeGeneric && p.use_tiles) {
-    const size_t t = tile::smem_bytes(p.d, p.dv);
+    while (p.tile_stages < tile::kMaxStages &&
+           tile::smem_bytes(p.d, p.dv, p.tile_stages + 1) <= budget)
+      ++p.tile_stages;
+    const size_t t = tile::smem_bytes(p.d, p.dv, p.tile_stages);
     if (t > smem) smem = t;
   }
   if (HasTiles<T>::v && mode == kModeFast) {
-    const size_t v = p.use_dec ? dec::smem_bytes() : vec::smem_bytes(p.d);
+    if (p.use_dec) {
+      while (p.dec_slots < dec::kMaxSlots && dec::smem_bytes(p.dec_slots + 1) <= budget)
+        ++p.dec_slots;
+    }
+    const size_t v = p.use_dec ? dec::smem_bytes(p.dec_slots) : vec::smem_bytes(p.d);
     if (v > smem) smem = v;
   }
   return smem;
 }
 
 template <typename T, int kMode>
-int launch_mode(const KParams& p, int32_t num_sms, int32_t ctas_per_sm, void* stream) {
-  const size_t smem = smem_for<T>(p, kMode);
+int launch_mode(const KParams& p_in, int32_t num_sms, int32_t ctas_per_sm, void* stream) {
+  KParams p = p_in;
+  const size_t smem = smem_for<T>(p, kMode, ctas_per_sm);
   cudaError_t e = cudaFuncSetAttribute(psa_persistent<T, kMode>,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
   if (e != cudaSuccess) return e;

@@ -64,6 +64,8 @@ struct KParams {
   int32_t use_vec_fast;  // bf16/f16, d == dv in {64, 128}: TMA-staged decode path
   int32_t trace_cap;     // diagnostics: capacity (items) of `trace`, 0 = off
   int32_t use_dec;       // VEC items on the tcgen05 decode pipeline (d == dv == 128)
+  int32_t tile_stages;   // TILE K/V ring depth (set by the launcher from the smem budget)
+  int32_t dec_slots;     // decode K/V ring slots (ditto)
   int32_t pad2;
   double scale;
   int64_t* trace;        // diagnostics: per item {cta | smid << 32, kind, t_start, t_end}

@@ -34,7 +34,7 @@ namespace tile {
 
 constexpr int kBN = 64;          // keys per KV block (S tile N)
 constexpr int kM = 128;          // rows per tile (UMMA M)
-constexpr int kStages = 2;
+constexpr int kMaxStages = 4;    // K/V ring depth: p.tile_stages (2 with 2 CTAs/SM, 4 with 1)
 constexpr uint32_t kTmemCols = 256;
 constexpr uint32_t kTmemS = 0;
 constexpr uint32_t kTmemP = 64;   // two P buffers: [64, 96) and [96, 128)
@@ -43,13 +43,13 @@ constexpr float kRescaleThreshold = 8.0f;  // log2 units
 
 struct Barriers {
   uint64_t q_full;
-  uint64_t k_full[kStages];
-  uint64_t v_full[kStages];
-  uint64_t k_empty[kStages];
-  uint64_t v_empty[kStages];
+  uint64_t k_full[kMaxStages];
+  uint64_t v_full[kMaxStages];
+  uint64_t k_empty[kMaxStages];
+  uint64_t v_empty[kMaxStages];
   uint64_t s_full;
   uint64_t s_free;
-  uint64_t p_full[kStages];  // per stage so a fast softmax can never lap the MMA waiter
+  uint64_t p_full[2];        // by block parity, so a fast softmax can never lap the MMA waiter
   uint64_t o_done[2];        // PV_n completes phase n >> 1 of o_done[n & 1]
 };
 
@@ -60,20 +60,21 @@ struct State {
   uint32_t tmem;    // TMEM base address
 };
 
-__host__ __device__ constexpr size_t smem_bytes(int d, int dv) {
+__host__ __device__ constexpr size_t smem_bytes(int d, int dv, int stages) {
   // Q + stages * (K + V) + 1 KB alignment slack
-  return size_t(kM) * d * 2 + size_t(kStages) * kBN * (d + dv) * 2 + 1024;
+  return size_t(kM) * d * 2 + size_t(stages) * kBN * (d + dv) * 2 + 1024;
 }
 
 __device__ __forceinline__ void init_barriers(Barriers* b) {
   dev::mbar_init(&b->q_full, 1);
-  for (int s = 0; s < kStages; ++s) {
+  for (int s = 0; s < kMaxStages; ++s) {
     dev::mbar_init(&b->k_full[s], 1);
     dev::mbar_init(&b->v_full[s], 1);
     dev::mbar_init(&b->k_empty[s], 1);
     dev::mbar_init(&b->v_empty[s], 1);
-    dev::mbar_init(&b->p_full[s], 4);
   }
+  dev::mbar_init(&b->p_full[0], 4);
+  dev::mbar_init(&b->p_full[1], 4);
   dev::mbar_init(&b->s_full, 1);
   dev::mbar_init(&b->s_free, 4);
   dev::mbar_init(&b->o_done[0], 1);
@@ -88,15 +89,17 @@ struct Layout {
   uint32_t q_bytes;  // kM * d * 2
   uint32_t k_bytes;  // kBN * d * 2
   uint32_t v_bytes;  // kBN * dv * 2
+  uint32_t stages;
   __device__ __forceinline__ uint8_t* q() const { return base; }
   __device__ __forceinline__ uint8_t* k(uint32_t s) const { return base + q_bytes + s * k_bytes; }
   __device__ __forceinline__ uint8_t* v(uint32_t s) const {
-    return base + q_bytes + kStages * k_bytes + s * v_bytes;
+    return base + q_bytes + stages * k_bytes + s * v_bytes;
   }
 };
 
-__device__ __forceinline__ Layout carve(uint8_t* smem_raw, int d, int dv) {
+__device__ __forceinline__ Layout carve(uint8_t* smem_raw, int d, int dv, int stages) {
   Layout L;
+  L.stages = uint32_t(stages);
   L.base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                       ~uintptr_t(1023));
   L.q_bytes = kM * d * 2;
@@ -162,7 +165,8 @@ __device__ __forceinline__ State tile_item(const KParams& p, const ItemT& it, ui
                                            Barriers* bar, State st) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int d = p.d, dv = p.dv;
-  const Layout L = carve(smem_raw, d, dv);
+  const Layout L = carve(smem_raw, d, dv, p.tile_stages);
+  const uint32_t NS = uint32_t(p.tile_stages);
   const int nbA = (it.pk1 - it.pk0 + kBN - 1) / kBN;
   const int nbB = (it.dk1 - it.dk0 + kBN - 1) / kBN;
   const int nb = nbA + nbB;
@@ -182,7 +186,7 @@ __device__ __forceinline__ State tile_item(const KParams& p, const ItemT& it, ui
       for (int c = 0; c < d / 64; ++c)
         dev::tma_load_4d(L.q() + c * (kM * 128), &p.tm_q, &bar->q_full, c * 64, 0, it.h, t_start);
       auto load_k = [&](int jb) {
-        const uint32_t n = base_blk + jb, s = n & 1, ph = (n >> 1) & 1;
+        const uint32_t n = base_blk + jb, s = n % NS, ph = (n / NS) & 1;
         const Block b = block_at(p, it, jb, nbA, pbase, dbase);
         dbg_event(p, st, kEvKWaitStart, jb);
         dev::mbar_wait(&bar->k_empty[s], ph ^ 1);  // S_{n-2} has consumed this stage
@@ -192,7 +196,7 @@ __device__ __forceinline__ State tile_item(const KParams& p, const ItemT& it, ui
           dev::tma_load_3d(L.k(s) + c * (kBN * 128), b.km, &bar->k_full[s], c * 64, it.h, b.key);
       };
       auto load_v = [&](int jb) {
-        const uint32_t n = base_blk + jb, s = n & 1, ph = (n >> 1) & 1;
+        const uint32_t n = base_blk + jb, s = n % NS, ph = (n / NS) & 1;
         const Block b = block_at(p, it, jb, nbA, pbase, dbase);
         dbg_event(p, st, kEvVWaitStart, jb);
         dev::mbar_wait(&bar->v_empty[s], ph ^ 1);  // PV_{n-2} has consumed this stage
@@ -219,8 +223,8 @@ __device__ __forceinline__ State tile_item(const KParams& p, const ItemT& it, ui
       dev::mbar_wait(&bar->q_full, st.items & 1);
       dev::tc_fence_after();
       auto issue_s = [&](int jb) {
-        const uint32_t n = base_blk + jb, s = n & 1;
-        dev::mbar_wait(&bar->k_full[s], (n >> 1) & 1);
+        const uint32_t n = base_blk + jb, s = n % NS;
+        dev::mbar_wait(&bar->k_full[s], (n / NS) & 1);
         dev::tc_fence_after();
         const uint32_t k_addr = dev::smem_u32(L.k(s));
         dbg_event(p, st, kEvSIssue, jb);
@@ -235,20 +239,20 @@ __device__ __forceinline__ State tile_item(const KParams& p, const ItemT& it, ui
       };
       issue_s(0);
       for (int jb = 0; jb < nb; ++jb) {
-        const uint32_t n = base_blk + jb, s = n & 1;
+        const uint32_t n = base_blk + jb, s = n % NS, pb = n & 1;
         if (jb + 1 < nb) {
           dev::mbar_wait(&bar->s_free, n & 1);  // S_n is in registers: S TMEM reusable
           dev::tc_fence_after();
           issue_s(jb + 1);
         }
-        dev::mbar_wait(&bar->p_full[s], (n >> 1) & 1);
-        dev::mbar_wait(&bar->v_full[s], (n >> 1) & 1);
+        dev::mbar_wait(&bar->p_full[pb], (n >> 1) & 1);
+        dev::mbar_wait(&bar->v_full[s], (n / NS) & 1);
         dev::tc_fence_after();
         const uint32_t v_addr = dev::smem_u32(L.v(s));
         dbg_event(p, st, kEvPvIssue, jb);
         for (int kk = 0; kk < kBN / 16; ++kk) {
           const uint64_t b = dev::umma_desc_sw128(v_addr + kk * (16 * 128), kBN * 128, 1024);
-          dev::mma_f16_ts(tO, tP + s * 32 + kk * 8, b, idesc_o, (jb > 0 || kk > 0));
+          dev::mma_f16_ts(tO, tP + pb * 32 + kk * 8, b, idesc_o, (jb > 0 || kk > 0));
         }
         dev::mma_commit(&bar->v_empty[s]);
         dev::mma_commit(&bar->o_done[n & 1]);
@@ -263,7 +267,7 @@ __device__ __forceinline__ State tile_item(const KParams& p, const ItemT& it, ui
     const float sc = float(p.scale) * 1.4426950408889634f;
     float m = -INFINITY, l = 0.f;
     for (int jb = 0; jb < nb; ++jb) {
-      const uint32_t n = base_blk + jb, s = n & 1;
+      const uint32_t n = base_blk + jb, s = n & 1;  // s: P buffer / p_full parity
       const Block b = block_at(p, it, jb, nbA, pbase, dbase);
       dev::mbar_wait(&bar->s_full, n & 1);
       if (threadIdx.x == 0) dbg_event(p, st, kEvSoftWait, jb);

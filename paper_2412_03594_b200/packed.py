@@ -215,7 +215,7 @@ class PrefixSharedAttention:
         (cta | smid << 32 | warp << 48, kind, t_start_ns, t_end_ns), rows in queue order;
         rows num_items + b hold CTA b's kernel start/end (kind -1)."""
         n = self.num_items + 4096  # items, then one residency record per CTA
-        buf = torch.zeros((n + 1024, 4), dtype=torch.int64, device=self.device)  # + tile events
+        buf = torch.zeros((n + 2048, 4), dtype=torch.int64, device=self.device)  # + tile/dec events
         L.check(L.lib().psa_debug_set_trace(_ptr(buf), n), "psa_debug_set_trace")
         try:
             self(*inputs)
@@ -224,6 +224,7 @@ class PrefixSharedAttention:
             L.lib().psa_debug_set_trace(None, 0)
         out = buf.cpu().numpy()
         self.last_tile_events = out[n:].reshape(-1)[:9 * 64].reshape(9, 64)
+        self.last_dec_events = out[n:].reshape(-1)[16 * 64:33 * 64].reshape(17, 64)
         ctas = out[self.num_items:n]
         return out[:self.num_items], ctas[ctas[:, 1] == -1]
 

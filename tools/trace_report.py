@@ -97,6 +97,13 @@ def main():
         rep["tile0_events_cycles"] = {nm: [int(x - t0) for x in ev[i, :nb]] for i, nm in enumerate(names) if nm != "misc"}
         rep["tile0_softmax_end"] = int(ev[5, 0] - t0)
         rep["tile0_item_end"] = int(ev[5, 1] - t0)
+    dv = getattr(op, "last_dec_events", None)
+    if dv is not None and dv[0, 0] != 0:
+        t0 = dv[0, 0]
+        nb = int((dv[2] != 0).sum())
+        names = ["k_issue", "v_issue", "s_issue", "pv_issue", "soft_s_ready", "p_arrive", "item_end", "epi_ofull_wait", "epi_ofull_done", "epi_finish_done", "ld_done", "max_done", "bar1_done", "exp_done", "odone_done", "pstore_done", "fence_done"]
+        rep["dec0_events_cycles"] = {nm: [int(x - t0) if x else 0 for x in dv[i, :min(nb, 16)]]
+                                     for i, nm in enumerate(names)}
     rep["config"] = args.config
     print(json.dumps(rep, indent=1))
     if args.json:
