@@ -45,7 +45,7 @@
 extern "C" {
 #endif
 
-#define PSA_ABI_VERSION 1
+#define PSA_ABI_VERSION 2
 
 typedef enum psa_status {
   PSA_OK = 0,
@@ -102,6 +102,9 @@ typedef struct psa_plan_opts {
   int32_t target_waves;   /* tile items per CTA the chunking aims at, 0 = default (1) */
   int32_t disable_vec_fast; /* 1 = VEC items on the generic CUDA-core path, 2 = on the warp-level
                                CUDA-core decode path instead of tcgen05 (diagnostics) */
+  int32_t kernel_variant;   /* 0 = auto: bf16/f16 with d == dv == 128 run the v2 kernel (one CTA
+                               per SM, 256-row paired tiles, prefill chunks fused with their own
+                               KV, two decode pipelines); 1 = the 2-CTA/SM kernel (diagnostics) */
 } psa_plan_opts;
 
 /* Read-only view of a plan's int32 tables (bit-exact with oracle/plan.py). */

@@ -49,9 +49,17 @@ def tiles_supported(dtype, d, dv, Hq, Hkv, disable_tiles=0):
     return Hq // Hkv <= TILE_M
 
 
+def v2_selected(dtype, d, dv, disable_vec_fast=0, kernel_variant=0):
+    """psa_plan_create's kernel choice: the v2 kernel (tile_pair, fuse_own, one CTA
+    per SM) for bf16/f16 with d == dv == 128 unless a diagnostic option opts out."""
+    return dtype in (1, 2) and d == 128 and dv == 128 and not disable_vec_fast \
+        and not kernel_variant
+
+
 def build_plan(G, R, Hq, Hkv, d, dv, dtype, cu_req, cu_q, cu_prefix, cu_distinct,
                num_sms=148, ctas_per_sm=2, tile_min_rows=32, disable_tiles=0,
-               min_chunk_keys=512, max_chunk_keys=16384, target_waves=1):
+               min_chunk_keys=512, max_chunk_keys=16384, target_waves=1, tile_pair=0,
+               fuse_own=0):
     """Returns dict(items, units, contribs, workspace_rows, chunk_keys, num_tile_items)."""
     cu_req = [int(x) for x in cu_req]
     cu_q = [int(x) for x in cu_q]
@@ -63,36 +71,67 @@ def build_plan(G, R, Hq, Hkv, d, dv, dtype, cu_req, cu_q, cu_prefix, cu_distinct
     elt = DTYPE_BYTES[dtype]
     width = d + dv
 
+    item_rows = 2 * tile_rows if tile_pair else tile_rows
+
     def kind_for(rows):
         return KIND_TILE if (tiles and rows >= tile_min_rows) else KIND_VEC
 
     def step_for(kind):
-        return tile_rows if kind == KIND_TILE else VEC_ROWS
+        return item_rows if kind == KIND_TILE else VEC_ROWS
 
-    total_vec = 0
-    tile_segs = []  # (row blocks x Hkv, keys)
+    # Row segments per group (psa_plan.cpp `Segment`): (row0, rows, req, P, D).
+    segs, sep = [], []
     for g in range(G):
         tok0 = cu_q[cu_req[g]]
         Ng = gqa * (cu_q[cu_req[g + 1]] - tok0)
         P = cu_prefix[g + 1] - cu_prefix[g]
-        if P > 0:
-            k = kind_for(Ng)
-            blocks = _cdiv(Ng, step_for(k))
+        sg, sp = [], []
+        if not fuse_own:
+            if P > 0:
+                sg.append((0, Ng, -1, P, 0))
+            sp = [r for r in range(cu_req[g], cu_req[g + 1]) if cu_distinct[r + 1] > cu_distinct[r]]
+        else:
+            run0 = -1
+            for r in range(cu_req[g], cu_req[g + 1]):
+                rb = gqa * (cu_q[r] - tok0)
+                nr = gqa * (cu_q[r + 1] - cu_q[r])
+                D = cu_distinct[r + 1] - cu_distinct[r]
+                if D > 0 and kind_for(nr) == KIND_TILE:
+                    if run0 >= 0 and P > 0:
+                        sg.append((run0, rb - run0, -1, P, 0))
+                    run0 = -1
+                    sg.append((rb, nr, r, P, D))
+                else:
+                    if run0 < 0:
+                        run0 = rb
+                    if D > 0:
+                        sp.append(r)
+            if run0 >= 0 and P > 0:
+                sg.append((run0, Ng - run0, -1, P, 0))
+        segs.append(sg)
+        sep.append(sp)
+
+    total_vec = 0
+    tile_segs = []  # (row blocks x Hkv, keys)
+    for g in range(G):
+        for (_r0, rows, _req, P, D) in segs[g]:
+            k = kind_for(rows)
+            blocks = _cdiv(rows, step_for(k))
             if k == KIND_TILE:
-                tile_segs.append((blocks * Hkv, P))
+                tile_segs.append((blocks * Hkv, P + D))
             else:
-                total_vec += blocks * P
-        for r in range(cu_req[g], cu_req[g + 1]):
+                total_vec += blocks * (P + D)
+        for r in sep[g]:
             D = cu_distinct[r + 1] - cu_distinct[r]
             nr = gqa * (cu_q[r + 1] - cu_q[r])
-            if D > 0:
-                k = kind_for(nr)
-                blocks = _cdiv(nr, step_for(k))
-                if k == KIND_TILE:
-                    tile_segs.append((blocks * Hkv, D))
-                else:
-                    total_vec += blocks * D
+            k = kind_for(nr)
+            blocks = _cdiv(nr, step_for(k))
+            if k == KIND_TILE:
+                tile_segs.append((blocks * Hkv, D))
+            else:
+                total_vec += blocks * D
     ctas = max(1, num_sms) * max(1, ctas_per_sm)
+    vec_ctas = max(1, num_sms) * 2 if tile_pair else ctas
     tile_target = ctas * max(1, target_waves)
 
     def tile_items(ck):
@@ -111,7 +150,7 @@ def build_plan(G, R, Hq, Hkv, d, dv, dtype, cu_req, cu_q, cu_prefix, cu_distinct
                 lo = mid + CHUNK_ALIGN
         lo = lo if tile_items(lo) <= tile_target else hi
     chunk = lo
-    vchunk = _cdiv(total_vec * Hkv, ctas * VEC_WARPS * VEC_WAVES)
+    vchunk = _cdiv(total_vec * Hkv, vec_ctas * VEC_WARPS * VEC_WAVES)
     vchunk = _rup(min(max(vchunk, CHUNK_ALIGN), VEC_MAX_KEYS), CHUNK_ALIGN)
 
     def per(L, kind):
@@ -123,7 +162,6 @@ def build_plan(G, R, Hq, Hkv, d, dv, dtype, cu_req, cu_q, cu_prefix, cu_distinct
     for g in range(G):
         tok0 = cu_q[cu_req[g]]
         Ng = gqa * (cu_q[cu_req[g + 1]] - tok0)
-        P = cu_prefix[g + 1] - cu_prefix[g]
         for h in range(Hkv):
             first = len(items)
 
@@ -136,16 +174,17 @@ def build_plan(G, R, Hq, Hkv, d, dv, dtype, cu_req, cu_q, cu_prefix, cu_distinct
                 it[IT_CANON] = len(items)
                 items.append(it)
 
-            if P > 0:
-                kind = kind_for(Ng)
-                step, pp = step_for(kind), per(P, kind)
-                for rb in range(0, Ng, step):
-                    for k0 in range(0, P, pp):
-                        push(kind, rb, min(step, Ng - rb), -1, k0, min(P, k0 + pp), 0, 0)
-            for r in range(cu_req[g], cu_req[g + 1]):
+            for (r0, rows, req, P, D) in segs[g]:
+                kind = kind_for(rows)
+                L = P + D
+                step, pp = step_for(kind), per(L, kind)
+                for o in range(0, rows, step):
+                    for k0 in range(0, L, pp):
+                        k1 = min(L, k0 + pp)
+                        push(kind, r0 + o, min(step, rows - o), req, min(k0, P), min(k1, P),
+                             max(k0 - P, 0), max(k1 - P, 0))
+            for r in sep[g]:
                 D = cu_distinct[r + 1] - cu_distinct[r]
-                if D <= 0:
-                    continue
                 rb = gqa * (cu_q[r] - tok0)
                 nr = gqa * (cu_q[r + 1] - cu_q[r])
                 kind = kind_for(nr)
@@ -157,6 +196,8 @@ def build_plan(G, R, Hq, Hkv, d, dv, dtype, cu_req, cu_q, cu_prefix, cu_distinct
             for it in items[first:]:
                 cuts.add(it[IT_ROW0])
                 cuts.add(it[IT_ROW0] + it[IT_ROWS])
+                if it[IT_KIND] == KIND_TILE and it[IT_ROWS] > tile_rows:
+                    cuts.add(it[IT_ROW0] + tile_rows)
             for r in range(cu_req[g], cu_req[g + 1]):
                 cuts.add(gqa * (cu_q[r] - tok0))
             cuts = sorted(cuts)
@@ -198,7 +239,8 @@ def build_plan(G, R, Hq, Hkv, d, dv, dtype, cu_req, cu_q, cu_prefix, cu_distinct
         keys = (it[IT_PK1] - it[IT_PK0]) + (it[IT_DK1] - it[IT_DK0])
         nbytes = (keys + it[IT_ROWS]) * width * elt
         if it[IT_KIND] == KIND_TILE:
-            cost.append(max(nbytes * BYTE_WEIGHT, 2 * TILE_M * keys * width))
+            slots = _cdiv(it[IT_ROWS], max(tile_rows, 1))
+            cost.append(max(nbytes * BYTE_WEIGHT, 2 * TILE_M * slots * keys * width))
         else:
             cost.append(max(nbytes * BYTE_WEIGHT,
                             2 * _rup(it[IT_ROWS], 4) * keys * width * VEC_FLOP_WEIGHT))

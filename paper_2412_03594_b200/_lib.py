@@ -17,6 +17,7 @@ LIB_PATH = os.path.join(_HERE, "libpsa.so")
 PSA_OK, PSA_INVALID_ARGUMENT, PSA_UNSUPPORTED, PSA_CUDA_ERROR = 0, 1, 2, 3
 DTYPE_F32, DTYPE_BF16, DTYPE_F16, DTYPE_F64 = 0, 1, 2, 3
 FLAG_PARTIAL_OUT = 1
+ABI_VERSION = 2  # include/psa.h PSA_ABI_VERSION
 
 
 class Problem(C.Structure):
@@ -39,6 +40,7 @@ class PlanOpts(C.Structure):
         ("num_sms", C.c_int32), ("ctas_per_sm", C.c_int32), ("tile_min_rows", C.c_int32),
         ("disable_tiles", C.c_int32), ("min_chunk_keys", C.c_int32),
         ("max_chunk_keys", C.c_int32), ("target_waves", C.c_int32), ("disable_vec_fast", C.c_int32),
+        ("kernel_variant", C.c_int32),
     ]
 
 

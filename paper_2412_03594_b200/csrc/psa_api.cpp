@@ -21,6 +21,7 @@ struct psa_plan {
   bool use_tiles = false;
   bool use_vec_fast = false;
   bool use_dec = false;
+  bool use_v2 = false;
   std::vector<int64_t> group_tok0, group_pbase, req_dbase;
   int64_t num_tokens = 0, prefix_keys = 0, distinct_keys = 0;
   // workspace layout (byte offsets)
@@ -136,6 +137,13 @@ psa_status psa_plan_create(const psa_problem* prob, const psa_plan_opts* opts, p
     st = current_sms(&o.num_sms);
     if (st != PSA_OK) return st;
   }
+  const bool v2 = psa::v2_supported(prob->dtype, prob->head_dim, prob->value_dim) &&
+                  !(opts && (opts->disable_vec_fast != 0 || opts->kernel_variant != 0));
+  if (v2) {
+    o.ctas_per_sm = 1;
+    o.tile_pair = 1;
+    o.fuse_own = 1;
+  }
   psa_plan* pl = new (std::nothrow) psa_plan();
   if (!pl) return fail(PSA_INVALID_ARGUMENT, "out of host memory");
   pl->dims = dims_of(prob);
@@ -151,6 +159,7 @@ psa_status psa_plan_create(const psa_problem* prob, const psa_plan_opts* opts, p
                      !(opts && opts->disable_vec_fast == 1);
   pl->use_dec = psa::dec_supported(prob->dtype, prob->head_dim, prob->value_dim) &&
                 !(opts && opts->disable_vec_fast == 2);
+  pl->use_v2 = v2;
   const auto& in = pl->dims;
   pl->group_tok0.resize(in.G);
   pl->group_pbase.resize(in.G);
@@ -260,9 +269,15 @@ psa_status psa_run(const psa_problem* prob, const psa_plan* pl, void* ws, size_t
   k.trace = g_trace;
   k.trace_cap = int32_t(g_trace_cap);
   k.use_tiles = pl->use_tiles ? 1 : 0;
-  k.use_vec_fast = (pl->use_vec_fast && !(prob->flags & PSA_FLAG_PARTIAL_OUT)) ? 1 : 0;
-  k.use_dec = (k.use_vec_fast && pl->use_dec) ? 1 : 0;
-  if (k.use_tiles || k.use_vec_fast || k.use_dec) {
+  k.use_v2 = pl->use_v2 ? 1 : 0;
+  if (pl->use_v2) {  // the v2 kernel handles PSA_FLAG_PARTIAL_OUT on both paths
+    k.use_vec_fast = 0;
+    k.use_dec = pl->plan.num_items > pl->plan.num_tile_items ? 1 : 0;
+  } else {
+    k.use_vec_fast = (pl->use_vec_fast && !(prob->flags & PSA_FLAG_PARTIAL_OUT)) ? 1 : 0;
+    k.use_dec = (k.use_vec_fast && pl->use_dec) ? 1 : 0;
+  }
+  if (k.use_tiles || k.use_vec_fast || k.use_dec || k.use_v2) {
     const uintptr_t align = reinterpret_cast<uintptr_t>(prob->q) |
                             reinterpret_cast<uintptr_t>(prob->k_prefix) |
                             reinterpret_cast<uintptr_t>(prob->v_prefix) |

@@ -38,6 +38,10 @@ constexpr float kRescaleThreshold = 8.0f;
 __host__ __device__ constexpr size_t smem_bytes(int slots) {
   return size_t(slots) * kSlotBytes + 2 * kQBytes + kPBytes + 1024;
 }
+// Offset between the shared-memory regions of two pipelines of one CTA.
+__host__ __device__ constexpr size_t pipe_stride(int slots) {
+  return (smem_bytes(slots) + 1023) & ~size_t(1023);
+}
 
 struct alignas(16) Shared {
   uint64_t slot_full[kMaxSlots], slot_empty[kMaxSlots];
@@ -116,8 +120,9 @@ __device__ __forceinline__ void dbg(const KParams& p, int ev, uint32_t g) {
   }
 }
 
-__device__ __forceinline__ void named_sync_softmax() {  // warps 0-3
-  asm volatile("bar.sync 1, 128;" ::: "memory");
+// Softmax warps of decode pipeline `pi` (barrier ids 4, 5: ids 1-3 belong to other phases).
+__device__ __forceinline__ void named_sync_softmax(int pi = 0) {
+  asm volatile("bar.sync %0, 128;" ::"r"(4 + pi) : "memory");
 }
 
 struct Geo {
@@ -161,11 +166,12 @@ __device__ __forceinline__ int block_nvalid(const ItemT& it, int nbA, int j) {
 }
 
 // The decode pipeline. `load(idx)` returns the ItemRec of queue entry idx;
-// `epilogue_out` / `arrive_merge` are provided by the kernel (output + merges).
+// `finish` / `merge_unit` are provided by the kernel (output + merges). Pipeline
+// `pi` runs on warps 8*pi .. 8*pi+7 (the v2 kernel runs two per CTA).
 template <typename T, typename LoadItem, typename Finish, typename MergeUnit>
-__device__ void run(const KParams& p, uint8_t* smem_raw, Shared* sh, uint32_t tmem,
+__device__ void run(const KParams& p, uint8_t* smem_raw, Shared* sh, uint32_t tmem, int pi,
                     LoadItem&& load_item_at, Finish&& finish, MergeUnit&& merge_unit) {
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int warp = (threadIdx.x >> 5) - 8 * pi, lane = threadIdx.x & 31;
   const Geo G = carve(smem_raw, p.dec_slots);
   const uint32_t NSL = uint32_t(p.dec_slots);
   const int n_items = p.num_items;
@@ -325,7 +331,7 @@ __device__ void run(const KParams& p, uint8_t* smem_raw, Shared* sh, uint32_t tm
     merge_loop(sh, merge_unit);
   } else if (warp < 4) {
     // ================= softmax + epilogue =================
-    const int t = threadIdx.x;
+    const int t = threadIdx.x - 256 * pi;
     const uint32_t lane_base = uint32_t(warp * 32) << 16;
     const uint32_t tS = tmem + kTmemS + lane_base;
     const float sc = float(p.scale) * 1.4426950408889634f;
@@ -383,7 +389,7 @@ __device__ void run(const KParams& p, uint8_t* smem_raw, Shared* sh, uint32_t tm
           for (int r = 0; r < kR; ++r) sh->red[g & 1][warp][r] = v[r];
         }
         if (t == 0) dbg(p, 11, g);
-        named_sync_softmax();  // red[g & 1] is rewritten two blocks later, after another barrier
+        named_sync_softmax(pi);  // red[g & 1] is rewritten two blocks later, after another barrier
         if (t == 0) dbg(p, 12, g);
         const float (&rd)[4][kR] = sh->red[g & 1];
         float alpha[kR];
@@ -451,7 +457,7 @@ __device__ void run(const KParams& p, uint8_t* smem_raw, Shared* sh, uint32_t tm
           for (int r = 0; r < kR; ++r) sh->red[g & 1][warp][r] = v[r];
         }
       }
-      named_sync_softmax();
+      named_sync_softmax(pi);
       float L[kR];
       {
         const float (&rd)[4][kR] = sh->red[g & 1];
@@ -474,7 +480,7 @@ __device__ void run(const KParams& p, uint8_t* smem_raw, Shared* sh, uint32_t tm
       for (int r = 0; r < kR; ++r) ov[r] = __uint_as_float(o[r]);
       finish(it, t, R, m, L, ov);  // writes output / partial, arrives at merge units
       if (t == 0) dbg(p, 9, g - 1);
-      named_sync_softmax();        // red[] reuse + item slot release after everyone finished
+      named_sync_softmax(pi);      // red[] reuse + item slot release after everyone finished
       if (t == 0) dev::mbar_arrive(&sh->item_empty[q]);
       if (t == 0) dbg(p, 6, g - 1);
       if (p.trace_cap > 0 && t == 0 && idx < p.trace_cap) {

@@ -18,6 +18,7 @@
 #include <cuda_fp16.h>
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cfloat>
 #include <cmath>
 #include <cstdint>
@@ -30,6 +31,7 @@
 #include "psa_tile.cuh"
 #include "psa_vec.cuh"
 #include "psa_dec.cuh"
+#include "psa_tile2.cuh"
 
 namespace psa {
 namespace {
@@ -662,6 +664,62 @@ __device__ __forceinline__ void warp_arrive_and_merge(const KParams& p, const It
   }
 }
 
+// End of a decode item (thread t = value column t of the item's <= 8 rows): the
+// partial rows + arrival at the merge units, or the final output.
+template <typename T>
+__device__ __forceinline__ void dec_finish(const KParams& p, dec::Shared* sh, const ItemRec& it,
+                                           int t, int R, const float (&m)[dec::kR],
+                                           const float (&L)[dec::kR], const float (&ov)[dec::kR],
+                                           int pi) {
+  if (it.ws_row >= 0) {
+    float* wo = static_cast<float*>(p.ws_o);
+#pragma unroll
+    for (int r = 0; r < dec::kR; ++r)
+      if (r < R) wo[((int64_t)it.ws_row + r) * 128 + t] = ov[r];
+    if (t == 0) {
+#pragma unroll
+      for (int r = 0; r < dec::kR; ++r)
+        if (r < R)
+          *reinterpret_cast<float2*>(static_cast<float*>(p.ws_ml) + ((int64_t)it.ws_row + r) * 2) =
+              make_float2(m[r], L[r]);
+    }
+    dec::named_sync_softmax(pi);
+    const int nu = it.u1 - it.u0;  // <= 9 units: one thread each
+    if (t < nu) {
+      const int u = it.u0 + t;
+      __threadfence();  // release: this item's partial rows (cumulative over the barrier)
+      const int need = __ldg(p.units + (int64_t)u * kUnitWords + kUnContribCount);
+      if (atomicAdd(p.unit_cnt + u, 1) == need - 1) {
+        p.unit_cnt[u] = 0;
+        dec::enqueue_merge(sh, u);
+      }
+    }
+    return;
+  }
+  const int64_t tok0 = __ldg(p.group_tok0 + it.g);
+  const bool partial_out = p.flags & PSA_FLAG_PARTIAL_OUT;
+#pragma unroll
+  for (int r = 0; r < dec::kR; ++r) {
+    if (r < R) {
+      const int row = it.row0 + r;
+      const int64_t idx = (tok0 + row / p.gqa) * p.Hq + (int64_t)it.h * p.gqa + row % p.gqa;
+      if (partial_out) {
+        static_cast<float*>(p.out)[idx * 128 + t] = ov[r];
+        if (t == 0) {
+          static_cast<float*>(p.m_out)[idx] = m[r] * Dom<float>::kToNat;
+          static_cast<float*>(p.l_out)[idx] = L[r];
+        }
+        continue;
+      }
+      static_cast<T*>(p.out)[idx * 128 + t] = from_acc<T>(ov[r] / L[r]);
+      if (t == 0) {
+        if (!(L[r] > 0.f)) atomicOr(&p.ctrl->error, 1);
+        if (p.lse) p.lse[idx] = (m[r] + log2f(L[r])) * Dom<float>::kToNat;
+      }
+    }
+  }
+}
+
 template <typename T, int kMode>
 __global__ void __launch_bounds__(kThreads, 2) psa_persistent(const __grid_constant__ KParams p) {
   using A = typename AccOf<T>::type;
@@ -776,47 +834,10 @@ __global__ void __launch_bounds__(kThreads, 2) psa_persistent(const __grid_const
       auto load_at = [&](int idx) { return load_item(p.items + (int64_t)idx * kItemWords); };
       auto finish = [&](const ItemRec& it, int t, int R, const float (&m)[dec::kR],
                         const float (&L)[dec::kR], const float (&ov)[dec::kR]) {
-        if (it.ws_row >= 0) {
-          float* wo = static_cast<float*>(p.ws_o);
-#pragma unroll
-          for (int r = 0; r < dec::kR; ++r)
-            if (r < R) wo[((int64_t)it.ws_row + r) * 128 + t] = ov[r];
-          if (t == 0) {
-#pragma unroll
-            for (int r = 0; r < dec::kR; ++r)
-              if (r < R)
-                *reinterpret_cast<float2*>(static_cast<float*>(p.ws_ml) + ((int64_t)it.ws_row + r) * 2) =
-                    make_float2(m[r], L[r]);
-          }
-          dec::named_sync_softmax();
-          const int nu = it.u1 - it.u0;  // <= 9 units: one thread each
-          if (t < nu) {
-            const int u = it.u0 + t;
-            __threadfence();  // release: this item's partial rows (cumulative over the barrier)
-            const int need = __ldg(p.units + (int64_t)u * kUnitWords + kUnContribCount);
-            if (atomicAdd(p.unit_cnt + u, 1) == need - 1) {
-              p.unit_cnt[u] = 0;
-              dec::enqueue_merge(&s_dec, u);
-            }
-          }
-        } else {
-          const int64_t tok0 = __ldg(p.group_tok0 + it.g);
-#pragma unroll
-          for (int r = 0; r < dec::kR; ++r) {
-            if (r < R) {
-              const int row = it.row0 + r;
-              const int64_t idx = (tok0 + row / p.gqa) * p.Hq + (int64_t)it.h * p.gqa + row % p.gqa;
-              static_cast<T*>(p.out)[idx * 128 + t] = from_acc<T>(ov[r] / L[r]);
-              if (t == 0) {
-                if (!(L[r] > 0.f)) atomicOr(&p.ctrl->error, 1);
-                if (p.lse) p.lse[idx] = (m[r] + log2f(L[r])) * Dom<float>::kToNat;
-              }
-            }
-          }
-        }
+        dec_finish<T>(p, &s_dec, it, t, R, m, L, ov, 0);
       };
       auto merge_u = [&](int u) { merge_unit_warp<T>(p, u); };
-      dec::run<T>(p, smem, &s_dec, tst.tmem, load_at, finish, merge_u);
+      dec::run<T>(p, smem, &s_dec, tst.tmem, 0, load_at, finish, merge_u);
     };
     if (dec_on) {
       cta_phase(p.n_tile_items);
@@ -852,6 +873,95 @@ __global__ void __launch_bounds__(kThreads, 2) psa_persistent(const __grid_const
     __syncthreads();
     if (warp == 5) dev::tmem_dealloc<tile::kTmemCols>(tst.tmem);
   }
+}
+
+// ---------------------------------------------------------------------------
+// v2 kernel (bf16/f16, d == dv == 128): ONE CTA per SM, 512 threads.
+//   tile phase  — tile2::run: two 128-row softmax slots share every K/V block
+//                 (warps 0-7 softmax, 8 producer, 9 MMA, 10-15 merges), all
+//                 512 TMEM columns;
+//   decode phase — two independent dec pipelines (warps 0-7 and 8-15), each
+//                 with its own K/V ring in one half of shared memory.
+// The tile phase drains the CTA-level TILE queue, the decode phase the VEC
+// queue; the last CTA out resets both cursors.
+// ---------------------------------------------------------------------------
+constexpr int kV2Threads = 512;
+constexpr int kV2EmuEvery = 4;  // every 4th exp pair of the tile softmax on the FMA pipe
+
+__device__ __forceinline__ void setmaxnreg_inc_184() { asm volatile("setmaxnreg.inc.sync.aligned.u32 184;"); }
+__device__ __forceinline__ void setmaxnreg_dec_72() { asm volatile("setmaxnreg.dec.sync.aligned.u32 72;"); }
+__device__ __forceinline__ void setmaxnreg_dec_128() { asm volatile("setmaxnreg.dec.sync.aligned.u32 128;"); }
+__device__ __forceinline__ void setmaxnreg_inc_128() { asm volatile("setmaxnreg.inc.sync.aligned.u32 128;"); }
+
+template <typename T>
+__global__ void __launch_bounds__(kV2Threads, 1) psa_v2(const __grid_constant__ KParams p) {
+  extern __shared__ __align__(1024) uint8_t smem[];
+  __shared__ tile2::Shared s_t2;
+  __shared__ dec::Shared s_dec[2];
+  __shared__ uint32_t s_tmem;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t t_kernel0 = (p.trace_cap > 0 && threadIdx.x == 0) ? int64_t(globaltimer()) : 0;
+  if (threadIdx.x == 0) {
+    tile2::init(&s_t2);
+    dec::init_barriers(&s_dec[0]);
+    dec::init_barriers(&s_dec[1]);
+  }
+  if (warp == tile2::kProducerWarp && lane == 0) {
+    if (p.use_tiles) dev::tma_prefetch_desc(&p.tm_q);
+    {
+      dev::tma_prefetch_desc(&p.tmd_kp);
+      dev::tma_prefetch_desc(&p.tmd_vp);
+      dev::tma_prefetch_desc(&p.tmd_kd);
+      dev::tma_prefetch_desc(&p.tmd_vd);
+    }
+  }
+  if (warp == tile2::kMmaWarp) dev::tmem_alloc<tile2::kTmemCols>(&s_tmem);
+  dev::tc_fence_before();
+  __syncthreads();
+  dev::tc_fence_after();
+  const uint32_t tmem = s_tmem;
+  auto load_at = [&](int idx) { return load_item(p.items + (int64_t)idx * kItemWords); };
+  auto merge_u = [&](int u) { merge_unit_warp<T>(p, u); };
+
+  if (p.use_tiles) {
+    if (warp < 8) {
+      setmaxnreg_inc_184();
+      tile2::run_softmax<T, kV2EmuEvery>(p, &s_t2, tmem, load_at);
+      setmaxnreg_dec_128();
+    } else {
+      setmaxnreg_dec_72();
+      if (warp >= tile2::kMergeWarp0) tile2::mq_loop(&s_t2.mq, 2, merge_u);
+      else tile2::run_support<T>(p, smem, &s_t2, tmem, load_at);
+      setmaxnreg_inc_128();
+    }
+    dev::tc_fence_before();
+    __syncthreads();
+    dev::tc_fence_after();
+  }
+  if (p.use_dec) {
+    const int pi = warp >> 3;
+    const size_t half = dec::pipe_stride(p.dec_slots);
+    auto finish = [&](const ItemRec& it, int t, int R, const float (&m)[dec::kR],
+                      const float (&L)[dec::kR], const float (&ov)[dec::kR]) {
+      dec_finish<T>(p, &s_dec[pi], it, t, R, m, L, ov, pi);
+    };
+    dec::run<T>(p, smem + pi * half, &s_dec[pi], tmem + 64u * uint32_t(pi), pi, load_at, finish,
+                merge_u);
+  }
+  __syncthreads();
+  if (p.trace_cap > 0 && threadIdx.x == 0) trace_item(p, p.num_items + int(blockIdx.x), -1, t_kernel0);
+  if (threadIdx.x == 0) {
+    __threadfence();
+    if (atomicAdd(&p.ctrl->done, 1) == (int)gridDim.x - 1) {
+      p.ctrl->next_item = 0;
+      p.ctrl->next_vec = 0;
+      p.ctrl->done = 0;
+      __threadfence();
+    }
+  }
+  dev::tc_fence_before();
+  __syncthreads();
+  if (warp == tile2::kMmaWarp) dev::tmem_dealloc<tile2::kTmemCols>(tmem);
 }
 
 // ---- standalone building blocks (PartialResult API) -----------------------
@@ -946,9 +1056,34 @@ int launch_mode(const KParams& p_in, int32_t num_sms, int32_t ctas_per_sm, void*
   return cudaGetLastError();
 }
 
+// v2: 227 KB of dynamic shared memory per CTA; the tile ring and the two decode
+// rings take as many 32 KB slots as fit.
+template <typename T>
+int launch_v2(const KParams& p_in, int32_t num_sms, void* stream) {
+  KParams p = p_in;
+  const size_t budget = size_t(227) * 1024 - 4 * 1024;  // minus static shared memory
+  p.tile_stages = 2;
+  while (p.tile_stages < tile2::kMaxRing && tile2::smem_bytes(p.tile_stages + 1) <= budget)
+    ++p.tile_stages;
+  p.dec_slots = 2;
+  while (p.dec_slots < dec::kMaxSlots && 2 * dec::pipe_stride(p.dec_slots + 1) <= budget)
+    ++p.dec_slots;
+  size_t smem = 0;
+  if (p.use_tiles) smem = tile2::smem_bytes(p.tile_stages);
+  if (p.use_dec) {
+    smem = std::max(smem, 2 * dec::pipe_stride(p.dec_slots));
+  }
+  cudaError_t e = cudaFuncSetAttribute(psa_v2<T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       int(smem));
+  if (e != cudaSuccess) return e;
+  psa_v2<T><<<num_sms, kV2Threads, smem, static_cast<cudaStream_t>(stream)>>>(p);
+  return cudaGetLastError();
+}
+
 template <typename T>
 int launch_typed(const KParams& p, int32_t num_sms, int32_t ctas_per_sm, void* stream) {
   if constexpr (HasTiles<T>::v) {
+    if (p.use_v2) return launch_v2<T>(p, num_sms, stream);
     if (p.use_vec_fast) return launch_mode<T, kModeFast>(p, num_sms, ctas_per_sm, stream);
     if (p.use_tiles) return launch_mode<T, kModeTileGeneric>(p, num_sms, ctas_per_sm, stream);
   }
@@ -1019,6 +1154,8 @@ bool dec_supported(int32_t dtype, int32_t d, int32_t dv) {
   return (dtype == PSA_DTYPE_BF16 || dtype == PSA_DTYPE_F16) && d == 128 && dv == 128;
 }
 
+bool v2_supported(int32_t dtype, int32_t d, int32_t dv) { return dec_supported(dtype, d, dv); }
+
 bool vec_fast_supported(int32_t dtype, int32_t d, int32_t dv) {
   return (dtype == PSA_DTYPE_BF16 || dtype == PSA_DTYPE_F16) && d == dv && (d == 64 || d == 128);
 }
@@ -1046,7 +1183,7 @@ int encode_tile_maps(KParams& p, int32_t dtype, int64_t T, int64_t prefix_keys,
     if (!e) e = encode_kv(&p.tm_kd, dt, p.kd, distinct_keys, p.Hkv, p.d, 64, tile::kBN, true);
     if (!e) e = encode_kv(&p.tm_vd, dt, p.vd, distinct_keys, p.Hkv, p.dv, 64, tile::kBN, true);
   }
-  if (!e && p.use_dec) {
+  if (!e && (p.use_dec || p.use_v2)) {
     e = encode_kv(&p.tmd_kp, dt, p.kp, prefix_keys, p.Hkv, p.d, 64, dec::kBK, true);
     if (!e) e = encode_kv(&p.tmd_vp, dt, p.vp, prefix_keys, p.Hkv, p.dv, 64, dec::kBK, true);
     if (!e) e = encode_kv(&p.tmd_kd, dt, p.kd, distinct_keys, p.Hkv, p.d, 64, dec::kBK, true);

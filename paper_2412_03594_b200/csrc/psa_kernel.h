@@ -66,7 +66,7 @@ struct KParams {
   int32_t use_dec;       // VEC items on the tcgen05 decode pipeline (d == dv == 128)
   int32_t tile_stages;   // TILE K/V ring depth (set by the launcher from the smem budget)
   int32_t dec_slots;     // decode K/V ring slots (ditto)
-  int32_t pad2;
+  int32_t use_v2;       // v2 kernel: 1 CTA/SM, paired tile slots + two decode pipelines
   double scale;
   int64_t* trace;        // diagnostics: per item {cta | smid << 32, kind, t_start, t_end}
 };
@@ -79,6 +79,8 @@ int encode_tile_maps(KParams& p, int32_t dtype, int64_t T, int64_t prefix_keys,
 bool vec_fast_supported(int32_t dtype, int32_t d, int32_t dv);
 // True when VEC items can run on the tcgen05 decode pipeline.
 bool dec_supported(int32_t dtype, int32_t d, int32_t dv);
+// True when the v2 kernel (1 CTA/SM: paired tcgen05 tiles + two decode pipelines) applies.
+bool v2_supported(int32_t dtype, int32_t d, int32_t dv);
 
 // Launches one persistent grid on `stream`. Returns a cudaError_t value.
 int launch_psa(const KParams& p, int32_t dtype, int32_t num_sms, int32_t ctas_per_sm,

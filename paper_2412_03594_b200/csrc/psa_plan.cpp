@@ -78,19 +78,59 @@ bool tiles_supported(const PlanInput& in, const PlanOptions& opt) {
   return (in.Hq / in.Hkv) <= kTileM;
 }
 
+// Row segments of one group (identical for every kv head). A segment is a run of
+// group rows evaluated against one key space: the prefix alone, or — with
+// fuse_own, for a request whose own rows go to TILE items — [prefix ++ that
+// request's distinct KV] in one online softmax (no merge between the two).
+struct Segment {
+  int64_t row0, rows;
+  int64_t req;  // -1: prefix-only run; else the request whose distinct KV is appended
+  int64_t P, D; // keys: P prefix keys, then D distinct keys of `req`
+};
+
 std::string build_plan(const PlanInput& in, const PlanOptions& opt, Plan* out) {
   std::string err = validate_offsets(in);
   if (!err.empty()) return err;
   const int64_t gqa = in.Hq / in.Hkv;
   const bool tiles = tiles_supported(in, opt);
   const int64_t tile_rows = tiles ? gqa * (kTileM / gqa) : 0;
+  const int64_t item_rows = opt.tile_pair ? 2 * tile_rows : tile_rows;
   const int64_t elt = dtype_bytes(in.dtype);
   const int64_t width = int64_t(in.d) + in.dv;
 
   auto kind_for = [&](int64_t rows) -> int32_t {
     return (tiles && rows >= opt.tile_min_rows) ? kItemTile : kItemVec;
   };
-  auto step_for = [&](int32_t kind) -> int64_t { return kind == kItemTile ? tile_rows : kVecRows; };
+  auto step_for = [&](int32_t kind) -> int64_t { return kind == kItemTile ? item_rows : kVecRows; };
+
+  // 0. Segments per group, and the requests whose distinct KV runs as separate items.
+  std::vector<std::vector<Segment>> segs(in.G);
+  std::vector<std::vector<int64_t>> sep(in.G);  // requests with separate distinct items
+  for (int32_t g = 0; g < in.G; ++g) {
+    const int64_t tok0 = in.cu_q[in.cu_req[g]];
+    const int64_t Ng = gqa * (in.cu_q[in.cu_req[g + 1]] - tok0);
+    const int64_t P = in.cu_prefix[g + 1] - in.cu_prefix[g];
+    if (!opt.fuse_own) {
+      if (P > 0) segs[g].push_back({0, Ng, -1, P, 0});
+      for (int64_t r = in.cu_req[g]; r < in.cu_req[g + 1]; ++r)
+        if (in.cu_distinct[r + 1] > in.cu_distinct[r]) sep[g].push_back(r);
+      continue;
+    }
+    int64_t run0 = -1;  // first row of the open prefix-only run
+    for (int64_t r = in.cu_req[g]; r < in.cu_req[g + 1]; ++r) {
+      const int64_t rb = gqa * (in.cu_q[r] - tok0), nr = gqa * (in.cu_q[r + 1] - in.cu_q[r]);
+      const int64_t D = in.cu_distinct[r + 1] - in.cu_distinct[r];
+      if (D > 0 && kind_for(nr) == kItemTile) {
+        if (run0 >= 0 && P > 0) segs[g].push_back({run0, rb - run0, -1, P, 0});
+        run0 = -1;
+        segs[g].push_back({rb, nr, r, P, D});
+      } else {
+        if (run0 < 0) run0 = rb;
+        if (D > 0) sep[g].push_back(r);
+      }
+    }
+    if (run0 >= 0 && P > 0) segs[g].push_back({run0, Ng - run0, -1, P, 0});
+  }
 
   // 1. Chunk sizes from the (row block x key) volume of each item kind.
   //    TILE items (CTA-level) aim at target_waves waves over all CTAs: every tile
@@ -100,28 +140,26 @@ std::string build_plan(const PlanInput& in, const PlanOptions& opt, Plan* out) {
   int64_t total_vec = 0;
   std::vector<std::pair<int64_t, int64_t>> tile_segs;  // (row blocks x Hkv, keys)
   for (int32_t g = 0; g < in.G; ++g) {
-    const int64_t tok0 = in.cu_q[in.cu_req[g]];
-    const int64_t Ng = gqa * (in.cu_q[in.cu_req[g + 1]] - tok0);
-    const int64_t P = in.cu_prefix[g + 1] - in.cu_prefix[g];
-    if (P > 0) {
-      const int32_t k = kind_for(Ng);
-      const int64_t blocks = ceil_div(Ng, step_for(k));
-      if (k == kItemTile) tile_segs.emplace_back(blocks * in.Hkv, P);
-      else total_vec += blocks * P;
+    for (const Segment& sg : segs[g]) {
+      const int32_t k = kind_for(sg.rows);
+      const int64_t blocks = ceil_div(sg.rows, step_for(k));
+      if (k == kItemTile) tile_segs.emplace_back(blocks * in.Hkv, sg.P + sg.D);
+      else total_vec += blocks * (sg.P + sg.D);
     }
-    for (int64_t r = in.cu_req[g]; r < in.cu_req[g + 1]; ++r) {
+    for (int64_t r : sep[g]) {
       const int64_t D = in.cu_distinct[r + 1] - in.cu_distinct[r];
       const int64_t nr = gqa * (in.cu_q[r + 1] - in.cu_q[r]);
-      if (D > 0) {
-        const int32_t k = kind_for(nr);
-        const int64_t blocks = ceil_div(nr, step_for(k));
-        if (k == kItemTile) tile_segs.emplace_back(blocks * in.Hkv, D);
-        else total_vec += blocks * D;
-      }
+      const int32_t k = kind_for(nr);
+      const int64_t blocks = ceil_div(nr, step_for(k));
+      if (k == kItemTile) tile_segs.emplace_back(blocks * in.Hkv, D);
+      else total_vec += blocks * D;
     }
   }
   total_vec *= in.Hkv;
   const int64_t ctas = int64_t(std::max(1, opt.num_sms)) * std::max(1, opt.ctas_per_sm);
+  // VEC queue consumers: warps of the legacy kernel, or the decode pipelines of the
+  // v2 kernel (two per CTA) — sized so both see the same chunking.
+  const int64_t vec_ctas = opt.tile_pair ? int64_t(std::max(1, opt.num_sms)) * 2 : ctas;
   // Tile chunk: the smallest multiple of kChunkAlign in [min, max] whose item count
   // fits target_waves waves of CTAs (binary search; item count is monotone).
   const int64_t tile_target = ctas * std::max(1, opt.target_waves);
@@ -141,7 +179,7 @@ std::string build_plan(const PlanInput& in, const PlanOptions& opt, Plan* out) {
     lo = tile_items(lo) <= tile_target ? lo : hi;
   }
   const int64_t chunk = lo;
-  int64_t vchunk = ceil_div(total_vec, ctas * kVecWarps * kVecWaves);
+  int64_t vchunk = ceil_div(total_vec, vec_ctas * kVecWarps * kVecWaves);
   vchunk = std::min<int64_t>(std::max<int64_t>(vchunk, kChunkAlign), kVecMaxKeys);
   vchunk = round_up(vchunk, kChunkAlign);
   const Chunking ck{chunk};
@@ -157,7 +195,6 @@ std::string build_plan(const PlanInput& in, const PlanOptions& opt, Plan* out) {
   for (int32_t g = 0; g < in.G; ++g) {
     const int64_t tok0 = in.cu_q[in.cu_req[g]];
     const int64_t Ng = gqa * (in.cu_q[in.cu_req[g + 1]] - tok0);
-    const int64_t P = in.cu_prefix[g + 1] - in.cu_prefix[g];
     for (int32_t h = 0; h < in.Hkv; ++h) {
       const size_t first = items.size();
       auto push = [&](int32_t kind, int64_t row0, int64_t rows, int64_t req, int64_t pk0,
@@ -172,16 +209,20 @@ std::string build_plan(const PlanInput& in, const PlanOptions& opt, Plan* out) {
         it[kItCanon] = int32_t(items.size());
         items.push_back(it);
       };
-      if (P > 0) {
-        const int32_t kind = kind_for(Ng);
-        const int64_t step = step_for(kind), per = (kind == kItemTile ? ck : ckv).per(P);
-        for (int64_t rb = 0; rb < Ng; rb += step)
-          for (int64_t k0 = 0; k0 < P; k0 += per)
-            push(kind, rb, std::min(step, Ng - rb), -1, k0, std::min(P, k0 + per), 0, 0);
+      for (const Segment& sg : segs[g]) {
+        const int32_t kind = kind_for(sg.rows);
+        const int64_t L = sg.P + sg.D;
+        const int64_t step = step_for(kind), per = (kind == kItemTile ? ck : ckv).per(L);
+        for (int64_t o = 0; o < sg.rows; o += step)
+          for (int64_t k0 = 0; k0 < L; k0 += per) {
+            const int64_t k1 = std::min(L, k0 + per);
+            push(kind, sg.row0 + o, std::min(step, sg.rows - o), sg.req, std::min(k0, sg.P),
+                 std::min(k1, sg.P), std::max<int64_t>(k0 - sg.P, 0),
+                 std::max<int64_t>(k1 - sg.P, 0));
+          }
       }
-      for (int64_t r = in.cu_req[g]; r < in.cu_req[g + 1]; ++r) {
+      for (int64_t r : sep[g]) {
         const int64_t D = in.cu_distinct[r + 1] - in.cu_distinct[r];
-        if (D <= 0) continue;
         const int64_t rb = gqa * (in.cu_q[r] - tok0), nr = gqa * (in.cu_q[r + 1] - in.cu_q[r]);
         const int32_t kind = kind_for(nr);
         const int64_t step = step_for(kind), per = (kind == kItemTile ? ck : ckv).per(D);
@@ -194,6 +235,9 @@ std::string build_plan(const PlanInput& in, const PlanOptions& opt, Plan* out) {
       for (size_t i = first; i < items.size(); ++i) {
         cuts.push_back(items[i][kItRow0]);
         cuts.push_back(int64_t(items[i][kItRow0]) + items[i][kItRows]);
+        // paired tiles: each 128-row slot arrives at its own units
+        if (items[i][kItKind] == kItemTile && items[i][kItRows] > tile_rows)
+          cuts.push_back(int64_t(items[i][kItRow0]) + tile_rows);
       }
       for (int64_t r = in.cu_req[g]; r < in.cu_req[g + 1]; ++r) cuts.push_back(gqa * (in.cu_q[r] - tok0));
       std::sort(cuts.begin(), cuts.end());
@@ -245,7 +289,8 @@ std::string build_plan(const PlanInput& in, const PlanOptions& opt, Plan* out) {
     const int64_t keys = int64_t(it[kItPk1] - it[kItPk0]) + (it[kItDk1] - it[kItDk0]);
     const int64_t bytes = (keys + it[kItRows]) * width * elt;
     if (it[kItKind] == kItemTile) {
-      cost[i] = std::max(bytes * kByteWeight, 2 * int64_t(kTileM) * keys * width);
+      const int64_t slots = ceil_div(it[kItRows], std::max<int64_t>(tile_rows, 1));
+      cost[i] = std::max(bytes * kByteWeight, 2 * int64_t(kTileM) * slots * keys * width);
     } else {
       cost[i] = std::max(bytes * kByteWeight, 2 * round_up(it[kItRows], 4) * keys * width * kVecFlopWeight);
     }

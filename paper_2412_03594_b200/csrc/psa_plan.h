@@ -56,6 +56,9 @@ struct PlanOptions {
   int32_t min_chunk_keys = 512;
   int32_t max_chunk_keys = 16384;
   int32_t target_waves = 1;
+  // v2 kernel (1 CTA/SM, two 128-row softmax slots sharing each K/V block):
+  int32_t tile_pair = 0;  // TILE items cover up to 2 x tile_rows rows (slot 0 + slot 1)
+  int32_t fuse_own = 0;   // a multi-token request's tiles run [prefix ++ own distinct] in one item
 };
 
 struct Plan {

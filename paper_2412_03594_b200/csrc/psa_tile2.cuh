@@ -1,0 +1,619 @@
+// psa_tile2.cuh — TILE work items of the v2 kernel (1 CTA per SM, 512 threads):
+// up to 256 stacked query rows of one (group, kv head) — two 128-row "slots" —
+// against one KV range, on the 5th-gen tensor cores. d == dv == 128, bf16/f16.
+//
+// This is the paper's §2.2 "matrix-vector -> matrix-matrix" transformation
+// (reference: the stacked prefix call, attention.py:174-179): all gqa heads x
+// tokens of a row range that share a KV range form the M rows of tcgen05 tiles,
+// so every K/V byte staged in shared memory feeds 256 rows. With fuse_own plans
+// a prefill-chunk request's tiles run over [prefix ++ own distinct KV] in one
+// online softmax (attention.py:187-198 merge folded into the block loop).
+//
+// Roles (warp = threadIdx.x / 32):
+//   warps 0-3   softmax WG0: slot 0, thread t = row t = TMEM lane t
+//   warps 4-7   softmax WG1: slot 1 (rows 128..255 of the item)
+//   warp 8      producer: pulls items (CTA-level queue), Q of both slots by TMA,
+//               then K_n, V_n blocks (128 keys) into a ring of 32 KB slots
+//   warp 9      MMA issuer (one lane): per block n and slot i,
+//                 O_i += P_{i,n-1} V_{n-1}   (A = P from TMEM, B = V MN-major)
+//                 S_i  = Q_i K_n^T           (A, B from smem, K-major)
+//   warps 10-15 merge workers for units this CTA completes
+// TMEM (512 columns): S0 [0,128), S1 [128,256), O0 [256,384), O1 [384,512).
+// P_i (bf16 pairs) overwrites S_i columns [0,64) in place; S_{i,n+1} is issued
+// after PV_{i,n}, and tcgen05 MMAs of one thread execute in issue order, so the
+// buffer is reused without a wait. The two slots ping-pong on the tensor core:
+// while WG0 exponentiates S_0 the MMA pipe computes slot 1, and vice versa.
+//
+// Online softmax (attention.py:95-98 per block, merge :101-119 across blocks)
+// runs in base 2 with a lazy rescale: O and l are rescaled only when a row's max
+// grows by more than 2^8 (the softmax WG rescales O_i in TMEM itself: s_full of
+// block n implies PV_{n-1} completed, and PV_n waits for this WG's p_full).
+// A fraction of the exponentials runs as a Cody-Waite + cubic polynomial on the
+// FMA pipe so MUFU.EX2 is not the only exp engine.
+#pragma once
+
+#include "psa_device.cuh"
+
+namespace psa {
+namespace tile2 {
+
+constexpr int kBN = 128;                  // keys per KV block (S tile N)
+constexpr int kM = 128;                   // rows per slot (UMMA M)
+constexpr int kD = 128;                   // d == dv
+constexpr int kSlotBytes = kBN * kD * 2;  // one K or V block: 32 KB
+constexpr int kQBytes = kM * kD * 2;      // one slot's Q tile: 32 KB
+constexpr int kMaxRing = 6;
+constexpr uint32_t kTmemCols = 512;
+constexpr uint32_t kTmemO = 256;
+constexpr float kRescaleThreshold = 8.0f;  // log2 units
+constexpr int kProducerWarp = 8, kMmaWarp = 9, kMergeWarp0 = 10;
+constexpr int kThreads = 512;
+
+// CTA-local merge queue: softmax threads append units whose last contribution
+// they delivered; merge warps drain it.
+struct MergeQ {
+  int mq[64];
+  int tail, head, done, closed, resv;
+};
+
+struct Shared {
+  uint64_t item_full[2], item_empty[2];
+  uint64_t q_full, q_empty;
+  uint64_t ring_full[kMaxRing], ring_empty[kMaxRing];
+  uint64_t s_full[2], p_full[2], o_full[2], o_empty[2];
+  int item_idx[2];
+  MergeQ mq;
+};
+
+__host__ __device__ constexpr size_t smem_bytes(int ring) {
+  return size_t(2) * kQBytes + size_t(ring) * kSlotBytes + 1024;
+}
+
+__device__ __forceinline__ void init(Shared* s) {
+  for (int i = 0; i < 2; ++i) {
+    dev::mbar_init(&s->item_full[i], 1);
+    dev::mbar_init(&s->item_empty[i], 3);  // MMA + WG0 + WG1
+    dev::mbar_init(&s->s_full[i], 1);
+    dev::mbar_init(&s->p_full[i], 4);
+    dev::mbar_init(&s->o_full[i], 1);
+    dev::mbar_init(&s->o_empty[i], 4);
+  }
+  dev::mbar_init(&s->q_full, 1);
+  dev::mbar_init(&s->q_empty, 1);
+  for (int i = 0; i < kMaxRing; ++i) {
+    dev::mbar_init(&s->ring_full[i], 1);
+    dev::mbar_init(&s->ring_empty[i], 1);
+  }
+  s->mq.tail = s->mq.head = s->mq.done = s->mq.closed = s->mq.resv = 0;
+  dev::fence_mbar_init();
+}
+
+__device__ __forceinline__ int ld_volatile(const int* p) { return *reinterpret_cast<const volatile int*>(p); }
+__device__ __forceinline__ void st_volatile(int* p, int v) { *reinterpret_cast<volatile int*>(p) = v; }
+
+__device__ __forceinline__ void mq_push(MergeQ* q, int u) {
+  const int slot = atomicAdd(&q->resv, 1);
+  while (slot - ld_volatile(&q->done) >= 64) __nanosleep(64);
+  st_volatile(&q->mq[slot & 63], u);
+  __threadfence_block();
+  while (ld_volatile(&q->tail) != slot) __nanosleep(32);  // publish in slot order
+  st_volatile(&q->tail, slot + 1);
+}
+
+// Merge warps: drain until `closers` producers closed the queue and it is empty.
+template <typename MergeUnit>
+__device__ __forceinline__ void mq_loop(MergeQ* q, int closers, MergeUnit&& merge_unit) {
+  const int lane = threadIdx.x & 31;
+  for (;;) {
+    int u = -1;
+    if (lane == 0) {
+      const int h = atomicAdd(&q->head, 1);
+      for (;;) {
+        if (h < ld_volatile(&q->tail)) { u = ld_volatile(&q->mq[h & 63]); break; }
+        if (ld_volatile(&q->closed) >= closers && h >= ld_volatile(&q->tail)) break;
+        __nanosleep(128);
+      }
+    }
+    u = __shfl_sync(0xffffffffu, u, 0);
+    if (u < 0) break;
+    __threadfence();  // acquire: the unit's partials were published before it was queued
+    merge_unit(u);
+    __syncwarp();
+    if (lane == 0) atomicAdd(&q->done, 1);
+  }
+}
+
+struct Geo {
+  uint8_t* base;  // 1024-aligned
+  uint32_t ring;
+  __device__ __forceinline__ uint8_t* q(int i) const { return base + i * kQBytes; }
+  __device__ __forceinline__ uint8_t* slot(uint32_t s) const { return base + 2 * kQBytes + s * kSlotBytes; }
+};
+
+__device__ __forceinline__ Geo carve(uint8_t* smem_raw, int ring) {
+  Geo g;
+  g.ring = uint32_t(ring);
+  g.base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                      ~uintptr_t(1023));
+  return g;
+}
+
+template <typename T> __device__ __forceinline__ uint32_t pack2(float a, float b);
+template <> __device__ __forceinline__ uint32_t pack2<__nv_bfloat16>(float a, float b) {
+  __nv_bfloat162 h = __floats2bfloat162_rn(a, b);
+  return *reinterpret_cast<uint32_t*>(&h);
+}
+template <> __device__ __forceinline__ uint32_t pack2<__half>(float a, float b) {
+  __half2 h = __floats2half2_rn(a, b);
+  return *reinterpret_cast<uint32_t*>(&h);
+}
+template <typename T> struct AbFormat;
+template <> struct AbFormat<__nv_bfloat16> { static constexpr uint32_t v = 1; };
+template <> struct AbFormat<__half> { static constexpr uint32_t v = 0; };
+
+__device__ __forceinline__ float max3(float a, float b, float c) {
+  float r;
+  asm("max.f32 %0, %1, %2, %3;" : "=f"(r) : "f"(a), "f"(b), "f"(c));
+  return r;
+}
+// (a0, a1) * (b, b) + (c, c) on the packed fp32x2 FMA path.
+__device__ __forceinline__ void ffma2(float& x0, float& x1, float a0, float a1, float b, float c) {
+  uint64_t r;
+  const uint64_t A = (uint64_t(__float_as_uint(a1)) << 32) | __float_as_uint(a0);
+  const uint64_t B = (uint64_t(__float_as_uint(b)) << 32) | __float_as_uint(b);
+  const uint64_t Cc = (uint64_t(__float_as_uint(c)) << 32) | __float_as_uint(c);
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(A), "l"(B), "l"(Cc));
+  x0 = __uint_as_float(uint32_t(r));
+  x1 = __uint_as_float(uint32_t(r >> 32));
+}
+__device__ __forceinline__ void fadd2(float& s0, float& s1, float a0, float a1) {
+  uint64_t r;
+  const uint64_t A = (uint64_t(__float_as_uint(a1)) << 32) | __float_as_uint(a0);
+  const uint64_t S = (uint64_t(__float_as_uint(s1)) << 32) | __float_as_uint(s0);
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(S), "l"(A));
+  s0 = __uint_as_float(uint32_t(r));
+  s1 = __uint_as_float(uint32_t(r >> 32));
+}
+
+// 2^x for x <= 0 on the FMA pipe (two lanes): clamp to -127, x = j + f with
+// j = round(x) (magic-number add), f in [-0.5, 0.5]; 2^f by a cubic
+// (max rel. error 7.5e-5, far below the bf16 rounding of P), 2^j by an exponent add.
+__device__ __forceinline__ void exp2_poly2(float& y0, float& y1, float x0, float x1) {
+  x0 = fmaxf(x0, -126.f);  // 2^j stays a (sub)normal exponent for j >= -126
+  x1 = fmaxf(x1, -126.f);
+  const float kMagic = 12582912.f;  // 1.5 * 2^23: t = x + kMagic holds round(x) in its low bits
+  float t0, t1, p0, p1;
+  ffma2(t0, t1, x0, x1, 1.f, kMagic);
+  float j0 = t0, j1 = t1;
+  fadd2(j0, j1, -kMagic, -kMagic);  // j = round(x)
+  float f0 = x0, f1 = x1;
+  fadd2(f0, f1, -j0, -j1);          // f = x - j in [-0.5, 0.5]
+  // minimax cubic for 2^f on [-0.5, 0.5]
+  const float c3 = 0.05517132f, c2 = 0.24261054f, c1 = 0.69326099f, c0 = 0.99992811f;
+  ffma2(p0, p1, f0, f1, c3, c2);
+  {
+    uint64_t r;
+    const uint64_t P = (uint64_t(__float_as_uint(p1)) << 32) | __float_as_uint(p0);
+    const uint64_t F = (uint64_t(__float_as_uint(f1)) << 32) | __float_as_uint(f0);
+    const uint64_t C1 = (uint64_t(__float_as_uint(c1)) << 32) | __float_as_uint(c1);
+    const uint64_t C0 = (uint64_t(__float_as_uint(c0)) << 32) | __float_as_uint(c0);
+    asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(P), "l"(F), "l"(C1));
+    asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(r), "l"(F), "l"(C0));
+    p0 = __uint_as_float(uint32_t(r));
+    p1 = __uint_as_float(uint32_t(r >> 32));
+  }
+  y0 = __uint_as_float(__float_as_uint(p0) + (__float_as_uint(t0) << 23));
+  y1 = __uint_as_float(__float_as_uint(p1) + (__float_as_uint(t1) << 23));
+}
+
+struct Block {
+  const CUtensorMap* km;
+  const CUtensorMap* vm;
+  int key;
+  int nvalid;
+};
+
+template <typename ItemT>
+__device__ __forceinline__ Block block_at(const KParams& p, const ItemT& it, int jb, int nbA,
+                                          int64_t pbase, int64_t dbase) {
+  Block b;
+  if (jb < nbA) {
+    b.km = &p.tmd_kp;  // (64, 1, 128)-key boxes, 128-byte swizzle
+    b.vm = &p.tmd_vp;
+    b.key = int(pbase + it.pk0 + jb * kBN);
+    b.nvalid = min(kBN, it.pk1 - it.pk0 - jb * kBN);
+  } else {
+    const int j = jb - nbA;
+    b.km = &p.tmd_kd;
+    b.vm = &p.tmd_vd;
+    b.key = int(dbase + it.dk0 + j * kBN);
+    b.nvalid = min(kBN, it.dk1 - it.dk0 - j * kBN);
+  }
+  return b;
+}
+
+template <typename ItemT>
+__device__ __forceinline__ void item_shape(const KParams& p, const ItemT& it, int& nbA, int& nb,
+                                           int64_t& pbase, int64_t& dbase) {
+  nbA = (it.pk1 - it.pk0 + kBN - 1) / kBN;
+  nb = nbA + (it.dk1 - it.dk0 + kBN - 1) / kBN;
+  pbase = nbA ? __ldg(p.group_pbase + it.g) : 0;
+  dbase = (it.dk1 > it.dk0 && it.req >= 0) ? __ldg(p.req_dbase + it.req) : 0;
+}
+
+__device__ __forceinline__ void named_sync(int id, int threads) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(threads) : "memory");
+}
+
+// ---------------------------------------------------------------------------
+// The tile phase. Returns when the TILE queue is drained and every role is done.
+//   load_item(idx)       -> ItemRec
+//   arrive(it, slot, r0, r1) : the slot's partial rows [r0, r1) are stored; the
+//                              WG (128 threads, after a named barrier) arrives at
+//                              the units inside that row range and queues merges
+//   merge_unit(u)        : merge worker body (one warp)
+// ---------------------------------------------------------------------------
+// Roles are separate functions so the kernel can call each inside its own
+// setmaxnreg region (ptxas sizes a region by the setmaxnreg that dominates it).
+template <typename T, typename LoadItem>
+__device__ void run_support(const KParams& p, uint8_t* smem_raw, Shared* sh, uint32_t tmem,
+                            LoadItem&& load_item_at) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const Geo G = carve(smem_raw, p.tile_stages);
+  const uint32_t NR = uint32_t(p.tile_stages);
+  const int gqa = p.gqa;
+  const int tile_rows = gqa * (kM / gqa);
+
+  if (warp == kProducerWarp) {
+    // ============================ producer ============================
+    uint32_t c = 0;  // ring loads issued
+    for (uint32_t k = 0;; ++k) {
+      const uint32_t q = k & 1;
+      dev::mbar_wait(&sh->item_empty[q], ((k >> 1) & 1) ^ 1);
+      int idx = 0;
+      if (lane == 0) idx = atomicAdd(&p.ctrl->next_item, 1);
+      idx = __shfl_sync(0xffffffffu, idx, 0);
+      if (idx >= p.n_tile_items) {
+        if (lane == 0) {
+          sh->item_idx[q] = -1;
+          dev::mbar_arrive(&sh->item_full[q]);
+        }
+        break;
+      }
+      if (lane == 0) {
+        sh->item_idx[q] = idx;
+        dev::mbar_arrive(&sh->item_full[q]);
+        const auto it = load_item_at(idx);
+        int nbA, nb;
+        int64_t pbase, dbase;
+        item_shape(p, it, nbA, nb, pbase, dbase);
+        const bool two = it.nrows > tile_rows;
+        // Q of both slots (the previous item's S MMAs have all completed)
+        dev::mbar_wait(&sh->q_empty, (k & 1) ^ 1);
+        const int t0 = int(__ldg(p.group_tok0 + it.g) + it.row0 / gqa);
+        const uint32_t qbox = uint32_t(tile_rows) * kD * 2;
+        dev::mbar_arrive_expect_tx(&sh->q_full, two ? 2 * qbox : qbox);
+        for (int i = 0; i < (two ? 2 : 1); ++i)
+          for (int ch = 0; ch < 2; ++ch)
+            dev::tma_load_4d(G.q(i) + ch * (kM * 128), &p.tm_q, &sh->q_full, ch * 64, 0, it.h,
+                             t0 + i * (kM / gqa));
+        for (int jb = 0; jb < nb; ++jb) {
+          const Block b = block_at(p, it, jb, nbA, pbase, dbase);
+          for (int w = 0; w < 2; ++w, ++c) {  // K_jb then V_jb
+            const uint32_t s = c % NR;
+            dev::mbar_wait(&sh->ring_empty[s], ((c / NR) & 1) ^ 1);
+            dev::mbar_arrive_expect_tx(&sh->ring_full[s], kSlotBytes);
+            const CUtensorMap* m = w == 0 ? b.km : b.vm;
+            dev::tma_load_3d(G.slot(s), m, &sh->ring_full[s], 0, it.h, b.key);
+            dev::tma_load_3d(G.slot(s) + kBN * 128, m, &sh->ring_full[s], 64, it.h, b.key);
+          }
+        }
+      }
+      __syncwarp();
+    }
+  } else if (warp == kMmaWarp) {
+    // ============================ MMA issuer ============================
+    if (lane == 0) {
+      constexpr uint32_t fmt = AbFormat<T>::v;
+      const uint32_t idesc_s = dev::umma_idesc_f16(fmt, kM, kBN, 0, 0);
+      const uint32_t idesc_o = dev::umma_idesc_f16(fmt, kM, kD, 0, 1);
+      uint32_t gb = 0;       // K/V blocks consumed (ring position 2 * gb)
+      uint32_t nblk[2] = {0u, 0u};  // blocks processed per slot (p_full phases)
+      uint32_t nitem[2] = {0u, 0u}; // items processed per slot (o_empty phases)
+      for (uint32_t k = 0;; ++k) {
+        const uint32_t q = k & 1;
+        dev::mbar_wait(&sh->item_full[q], (k >> 1) & 1);
+        const int idx = sh->item_idx[q];
+        if (idx < 0) break;
+        const auto it = load_item_at(idx);
+        dev::mbar_arrive(&sh->item_empty[q]);
+        int nbA, nb;
+        int64_t pbase, dbase;
+        item_shape(p, it, nbA, nb, pbase, dbase);
+        const int ns = it.nrows > tile_rows ? 2 : 1;
+        dev::mbar_wait(&sh->q_full, k & 1);
+        dev::tc_fence_after();
+        auto issue_pv = [&](int i, uint32_t vslot, bool first) {
+          // O_i (+)= P_i V: 8 K-steps of 16 keys; A = P_i in TMEM (bf16 pairs)
+          const uint32_t v_addr = dev::smem_u32(G.slot(vslot));
+          const uint32_t tP = tmem + uint32_t(i) * 128, tO = tmem + kTmemO + uint32_t(i) * 128;
+#pragma unroll
+          for (int kk = 0; kk < kBN / 16; ++kk) {
+            const uint64_t b = dev::umma_desc_sw128(v_addr + kk * (16 * 128), kBN * 128, 1024);
+            dev::mma_f16_ts(tO, tP + kk * 8, b, idesc_o, (!first || kk > 0) ? 1u : 0u);
+          }
+        };
+        auto issue_s = [&](int i, uint32_t kslot) {
+          const uint32_t k_addr = dev::smem_u32(G.slot(kslot));
+          const uint32_t q_addr = dev::smem_u32(G.q(i));
+          const uint32_t tS = tmem + uint32_t(i) * 128;
+#pragma unroll
+          for (int kk = 0; kk < kD / 16; ++kk) {
+            const uint32_t ch = kk >> 2, w = (kk & 3) * 32;
+            const uint64_t a = dev::umma_desc_sw128(q_addr + ch * (kM * 128) + w, 16, 1024);
+            const uint64_t b = dev::umma_desc_sw128(k_addr + ch * (kBN * 128) + w, 16, 1024);
+            dev::mma_f16_ss(tS, a, b, idesc_s, kk > 0 ? 1u : 0u);
+          }
+          dev::mma_commit(&sh->s_full[i]);
+        };
+        for (int n = 0; n < nb; ++n) {
+          const uint32_t cK = 2 * (gb + n), sK = cK % NR;
+          const uint32_t cV = cK - 1, sV = cV % NR;  // V_{n-1}
+          dev::mbar_wait(&sh->ring_full[sK], (cK / NR) & 1);
+          if (n > 0) dev::mbar_wait(&sh->ring_full[sV], (cV / NR) & 1);
+          dev::tc_fence_after();
+          for (int i = 0; i < ns; ++i) {
+            if (n > 0) {
+              if (n == 1) {  // first PV of this item overwrites O_i: the WG read the last one
+                dev::mbar_wait(&sh->o_empty[i], (nitem[i] & 1) ^ 1);
+              }
+              dev::mbar_wait(&sh->p_full[i], nblk[i] & 1);
+              ++nblk[i];
+              dev::tc_fence_after();
+              issue_pv(i, sV, n == 1);
+            }
+            issue_s(i, sK);
+          }
+          if (n > 0) dev::mma_commit(&sh->ring_empty[sV]);
+          dev::mma_commit(&sh->ring_empty[sK]);
+        }
+        dev::mma_commit(&sh->q_empty);  // every S of this item issued
+        {
+          const uint32_t cV = 2 * (gb + nb) - 1, sV = cV % NR;
+          dev::mbar_wait(&sh->ring_full[sV], (cV / NR) & 1);
+          for (int i = 0; i < ns; ++i) {
+            if (nb == 1) dev::mbar_wait(&sh->o_empty[i], (nitem[i] & 1) ^ 1);
+            dev::mbar_wait(&sh->p_full[i], nblk[i] & 1);
+            ++nblk[i];
+            dev::tc_fence_after();
+            issue_pv(i, sV, nb == 1);
+            dev::mma_commit(&sh->o_full[i]);
+            ++nitem[i];
+          }
+          dev::mma_commit(&sh->ring_empty[sV]);
+        }
+        gb += nb;
+      }
+    }
+  }
+}
+
+template <typename T, int kEmuEvery, typename LoadItem>
+__device__ void run_softmax(const KParams& p, Shared* sh, uint32_t tmem, LoadItem&& load_item_at) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int gqa = p.gqa;
+  const int tile_rows = gqa * (kM / gqa);
+  {
+    // ============================ softmax WG i ============================
+    const int i = warp >> 2;
+    const int row = threadIdx.x & 127;
+    const uint32_t lane_base = uint32_t((warp & 3) * 32) << 16;
+    const uint32_t tS = tmem + uint32_t(i) * 128 + lane_base;
+    const uint32_t tO = tmem + kTmemO + uint32_t(i) * 128 + lane_base;
+    const float sc = float(p.scale) * 1.4426950408889634f;
+    uint32_t nblk = 0, nitem = 0;
+    for (uint32_t k = 0;; ++k) {
+      const uint32_t q = k & 1;
+      dev::mbar_wait(&sh->item_full[q], (k >> 1) & 1);
+      const int idx = sh->item_idx[q];
+      if (idx < 0) break;
+      const auto it = load_item_at(idx);
+      named_sync(2 + i, 128);  // every thread of the WG has read item_idx[q]
+      if (threadIdx.x % 128 == 0) dev::mbar_arrive(&sh->item_empty[q]);
+      const int slot_rows = i == 0 ? min(it.nrows, tile_rows) : it.nrows - tile_rows;
+      if (slot_rows <= 0) continue;
+      int nbA, nb;
+      int64_t pbase, dbase;
+      item_shape(p, it, nbA, nb, pbase, dbase);
+      float m = -INFINITY, l0 = 0.f, l1 = 0.f;
+      for (int n = 0; n < nb; ++n, ++nblk) {
+        const int nvalid = n < nbA ? min(kBN, it.pk1 - it.pk0 - n * kBN)
+                                   : min(kBN, it.dk1 - it.dk0 - (n - nbA) * kBN);
+        dev::mbar_wait(&sh->s_full[i], nblk & 1);
+        dev::tc_fence_after();
+        uint32_t r[4][32];
+        dev::tmem_ld32(tS + 0, r[0]);
+        dev::tmem_ld32(tS + 32, r[1]);
+        dev::tmem_ld32(tS + 64, r[2]);
+        dev::tmem_ld32(tS + 96, r[3]);
+        dev::tmem_wait_ld();
+        if (nvalid < kBN) {
+#pragma unroll
+          for (int c = 0; c < 4; ++c)
+#pragma unroll
+            for (int e = 0; e < 32; ++e)
+              if (c * 32 + e >= nvalid) r[c][e] = 0xff800000u;
+        }
+        // row max of the raw scores (scale > 0): 8 independent FMNMX3 chains
+        float a8[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          const uint32_t* v = &r[j >> 1][(j & 1) * 16];
+          float acc = fmaxf(__uint_as_float(v[0]), __uint_as_float(v[1]));
+#pragma unroll
+          for (int e = 2; e < 16; e += 2) acc = max3(acc, __uint_as_float(v[e]), __uint_as_float(v[e + 1]));
+          a8[j] = acc;
+        }
+        const float mraw = max3(max3(a8[0], a8[1], a8[2]), max3(a8[3], a8[4], a8[5]), fmaxf(a8[6], a8[7]));
+        const float mb = mraw * sc;
+        float alpha = 1.f;
+        bool rescale = false;
+        if (m == -INFINITY) {
+          m = mb;
+        } else if (mb > m + kRescaleThreshold) {
+          alpha = dev::ex2(m - mb);
+          m = mb;
+          rescale = true;
+        }
+        l0 *= alpha;
+        l1 *= alpha;
+        const float nm = -m;
+        // P = 2^(s*sc - m), packed bf16 pairs into r[c][0..15]; sums in (l0, l1)
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+#pragma unroll
+          for (int e = 0; e < 16; ++e) {
+            float x0, x1, y0, y1;
+            ffma2(x0, x1, __uint_as_float(r[c][2 * e]), __uint_as_float(r[c][2 * e + 1]), sc, nm);
+            if (kEmuEvery > 0 && ((c * 16 + e) % kEmuEvery) == kEmuEvery - 1) {
+              exp2_poly2(y0, y1, x0, x1);
+            } else {
+              y0 = dev::ex2(x0);
+              y1 = dev::ex2(x1);
+            }
+            fadd2(l0, l1, y0, y1);
+            r[c][e] = pack2<T>(y0, y1);
+          }
+        }
+        // P_n -> S_i columns [0, 64)
+        {
+          uint32_t hi[32];
+#pragma unroll
+          for (int e = 0; e < 16; ++e) { hi[e] = r[2][e]; hi[16 + e] = r[3][e]; }
+          uint32_t lo[32];
+#pragma unroll
+          for (int e = 0; e < 16; ++e) { lo[e] = r[0][e]; lo[16 + e] = r[1][e]; }
+          dev::tmem_st32(tS + 0, lo);
+          dev::tmem_st32(tS + 32, hi);
+        }
+        if (__any_sync(0xffffffffu, rescale)) {
+          // O_i holds PV_0..PV_{n-1} (complete: S_n was issued after PV_{n-1}, and
+          // PV_n waits for this WG's p_full)
+#pragma unroll 1
+          for (int c = 0; c < kD; c += 32) {
+            uint32_t o[32];
+            dev::tmem_ld32(tO + c, o);
+            dev::tmem_wait_ld();
+#pragma unroll
+            for (int e = 0; e < 32; ++e) o[e] = __float_as_uint(__uint_as_float(o[e]) * alpha);
+            dev::tmem_st32(tO + c, o);
+          }
+        }
+        dev::tmem_wait_st();
+        dev::tc_fence_before();
+        __syncwarp();
+        if (lane == 0) dev::mbar_arrive(&sh->p_full[i]);
+      }
+      // ---------------- epilogue: O_i -> output / partial ----------------
+      dev::mbar_wait(&sh->o_full[i], nitem & 1);
+      ++nitem;
+      dev::tc_fence_after();
+      const float l = l0 + l1;
+      const int slot_row0 = it.row0 + i * tile_rows;
+      const bool valid = row < slot_rows;
+      const bool partial_out = p.flags & PSA_FLAG_PARTIAL_OUT;
+      if (it.ws_row >= 0) {
+        float* wo = static_cast<float*>(p.ws_o) + ((int64_t)it.ws_row + i * tile_rows + row) * kD;
+#pragma unroll 1
+        for (int c = 0; c < kD; c += 32) {
+          uint32_t o[32];
+          dev::tmem_ld32(tO + c, o);
+          dev::tmem_wait_ld();
+          if (c == kD - 32) {
+            dev::tc_fence_before();
+            __syncwarp();
+            if (lane == 0) dev::mbar_arrive(&sh->o_empty[i]);
+          }
+          if (valid) {
+#pragma unroll
+            for (int e = 0; e < 32; e += 4)
+              *reinterpret_cast<float4*>(wo + c + e) =
+                  make_float4(__uint_as_float(o[e]), __uint_as_float(o[e + 1]),
+                              __uint_as_float(o[e + 2]), __uint_as_float(o[e + 3]));
+          }
+        }
+        if (valid)
+          *reinterpret_cast<float2*>(static_cast<float*>(p.ws_ml) +
+                                     ((int64_t)it.ws_row + i * tile_rows + row) * 2) = make_float2(m, l);
+        // publish the slot's partial rows, then arrive at the units they cover
+        named_sync(2 + i, 128);
+        const int32_t* U = p.units;
+        const int r0 = slot_row0, r1 = slot_row0 + slot_rows;
+        for (int u = it.u0 + (threadIdx.x & 127); u < it.u1; u += 128) {
+          const int ur0 = __ldg(U + (int64_t)u * kUnitWords + kUnRow0);
+          if (ur0 < r0 || ur0 >= r1) continue;
+          __threadfence();
+          const int need = __ldg(U + (int64_t)u * kUnitWords + kUnContribCount);
+          if (atomicAdd(p.unit_cnt + u, 1) == need - 1) {
+            p.unit_cnt[u] = 0;
+            mq_push(&sh->mq, u);
+          }
+        }
+      } else {
+        const int grow = slot_row0 + row;
+        const int64_t tok = __ldg(p.group_tok0 + it.g) + grow / gqa;
+        const int64_t oidx = tok * p.Hq + (int64_t)it.h * gqa + grow % gqa;
+        const float inv = 1.f / l;
+#pragma unroll 1
+        for (int c = 0; c < kD; c += 32) {
+          uint32_t o[32];
+          dev::tmem_ld32(tO + c, o);
+          dev::tmem_wait_ld();
+          if (c == kD - 32) {
+            dev::tc_fence_before();
+            __syncwarp();
+            if (lane == 0) dev::mbar_arrive(&sh->o_empty[i]);
+          }
+          if (!valid) continue;
+          if (partial_out) {
+            float* dst = static_cast<float*>(p.out) + oidx * kD + c;
+#pragma unroll
+            for (int e = 0; e < 32; e += 4)
+              *reinterpret_cast<float4*>(dst + e) =
+                  make_float4(__uint_as_float(o[e]), __uint_as_float(o[e + 1]),
+                              __uint_as_float(o[e + 2]), __uint_as_float(o[e + 3]));
+          } else {
+            uint8_t* dst = reinterpret_cast<uint8_t*>(static_cast<T*>(p.out) + oidx * kD + c);
+#pragma unroll
+            for (int e = 0; e < 32; e += 8) {
+              uint4 v;
+              v.x = pack2<T>(__uint_as_float(o[e]) * inv, __uint_as_float(o[e + 1]) * inv);
+              v.y = pack2<T>(__uint_as_float(o[e + 2]) * inv, __uint_as_float(o[e + 3]) * inv);
+              v.z = pack2<T>(__uint_as_float(o[e + 4]) * inv, __uint_as_float(o[e + 5]) * inv);
+              v.w = pack2<T>(__uint_as_float(o[e + 6]) * inv, __uint_as_float(o[e + 7]) * inv);
+              *reinterpret_cast<uint4*>(dst + e * 2) = v;
+            }
+          }
+        }
+        if (valid) {
+          if (partial_out) {
+            static_cast<float*>(p.m_out)[oidx] = m * 0.6931471805599453f;
+            static_cast<float*>(p.l_out)[oidx] = l;
+          } else {
+            if (!(l > 0.f)) atomicOr(&p.ctrl->error, 1);
+            if (p.lse) p.lse[oidx] = (m + log2f(l)) * 0.6931471805599453f;
+          }
+        }
+      }
+    }
+    // this WG will not queue more merges
+    named_sync(2 + i, 128);
+    if ((threadIdx.x & 127) == 0) {
+      __threadfence_block();
+      atomicAdd(&sh->mq.closed, 1);
+    }
+  }
+}
+
+}  // namespace tile2
+}  // namespace psa

@@ -67,11 +67,12 @@ class PlanOptions:
     max_chunk_keys: int = 0
     target_waves: int = 0
     disable_vec_fast: int = 0
+    kernel_variant: int = 0  # 0 = auto (v2 for bf16/f16 d=dv=128), 1 = 2-CTA/SM kernel
 
     def to_c(self) -> L.PlanOpts:
         return L.PlanOpts(self.num_sms, self.ctas_per_sm, self.tile_min_rows, self.disable_tiles,
                           self.min_chunk_keys, self.max_chunk_keys, self.target_waves,
-                          self.disable_vec_fast)
+                          self.disable_vec_fast, self.kernel_variant)
 
 
 class PrefixSharedAttention:

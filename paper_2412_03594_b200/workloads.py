@@ -86,7 +86,16 @@ def config(name: str) -> Spec:
     if name == "c2_decode":
         return Spec("c2_decode", 32, 8, 128, 128, "bf16", "normal", [0] * 16,
                     [[(1, 256)] * 32 for _ in range(16)], seed=2)
-    raise ValueError(f"unknown config {name!r} (c1..c5, c2_prefix, c2_decode)")
+    # diagnostic parts of c3: the prefix tiles alone / the prefill chunks' own KV alone
+    if name == "c3_prefix":
+        reqs = [(1, 0)] * 16 + [(512, 0)] + [(1, 0)] * 16 + [(512, 0)]
+        return Spec("c3_prefix", 32, 8, 128, 128, "bf16", "normal", [2048] * 64,
+                    [list(reqs) for _ in range(64)], seed=3)
+    if name == "c3_chunks":
+        return Spec("c3_chunks", 32, 8, 128, 128, "bf16", "normal", [0] * 64,
+                    [[(512, 512)] * 2 for _ in range(64)], seed=3)
+    raise ValueError(f"unknown config {name!r} (c1..c5, c2_prefix, c2_decode, c3_prefix, "
+                     "c3_chunks)")
 
 
 def offsets(spec: Spec) -> dict:

@@ -1,6 +1,7 @@
 """The C-ABI library loads (no GPU needed) and exports every symbol include/psa.h declares."""
 
 import ctypes
+import pytest
 import os
 import re
 
@@ -32,7 +33,7 @@ def test_library_exports_every_declared_symbol():
 
 def test_abi_version_and_error_channel():
     lib = L.lib()
-    assert lib.psa_abi_version() == 1
+    assert lib.psa_abi_version() == 2  # psa_plan_opts.kernel_variant
     # a NULL problem is rejected with INVALID_ARGUMENT and a message, no CUDA needed
     h = ctypes.c_void_p()
     st = lib.psa_plan_create(None, None, ctypes.byref(h))
@@ -40,9 +41,22 @@ def test_abi_version_and_error_channel():
     assert "NULL" in L.last_error()
 
 
-def test_struct_sizes_match_header_layout():
+def test_struct_sizes_match_header_layout(tmp_path):
     # psa_problem: 8 int32 + double + 4 offset ptrs + 9 buffer ptrs = 32 + 8 + 104 on LP64
-    # (cross-checked against gcc's sizeof of include/psa.h)
     assert ctypes.sizeof(L.Problem) == 144
-    assert ctypes.sizeof(L.PlanOpts) == 32
+    assert ctypes.sizeof(L.PlanOpts) == 36
     assert ctypes.sizeof(L.PlanView) == 56
+    # cross-check against the C compiler's view of include/psa.h
+    import shutil
+    import subprocess
+    cc = shutil.which("gcc") or shutil.which("cc")
+    if cc is None:
+        pytest.skip("no C compiler")
+    inc = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "include")
+    src = tmp_path / "sz.c"
+    src.write_text('#include <stdio.h>\n#include "psa.h"\nint main(void){printf("%zu %zu %zu", '
+                   'sizeof(psa_problem), sizeof(psa_plan_opts), sizeof(psa_plan_view));return 0;}\n')
+    exe = tmp_path / "sz"
+    subprocess.run([cc, "-I", inc, str(src), "-o", str(exe)], check=True)
+    got = [int(x) for x in subprocess.run([str(exe)], capture_output=True, text=True).stdout.split()]
+    assert got == [ctypes.sizeof(L.Problem), ctypes.sizeof(L.PlanOpts), ctypes.sizeof(L.PlanView)]

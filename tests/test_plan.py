@@ -26,9 +26,11 @@ def _compare(off, Hq, Hkv, d, dv, dt, **opt):
     opts = P.PlanOptions(**{"num_sms": 148, **opt})
     got = P.plan_tables_host(off["cu_req"], off["cu_q"], off["cu_prefix"], off["cu_distinct"],
                              Hq, Hkv, d, dv, tdt, opts)
+    v2 = OP.v2_selected(pdt, d, dv, opts.disable_vec_fast, opts.kernel_variant)
     want = OP.build_plan(len(off["cu_req"]) - 1, len(off["cu_q"]) - 1, Hq, Hkv, d, dv, pdt,
                          off["cu_req"], off["cu_q"], off["cu_prefix"], off["cu_distinct"],
-                         num_sms=opts.num_sms, ctas_per_sm=opts.ctas_per_sm or 2,
+                         num_sms=opts.num_sms, ctas_per_sm=1 if v2 else (opts.ctas_per_sm or 2),
+                         tile_pair=int(v2), fuse_own=int(v2),
                          tile_min_rows=opts.tile_min_rows or 32,
                          disable_tiles=opts.disable_tiles,
                          min_chunk_keys=opts.min_chunk_keys or 512,
@@ -48,16 +50,18 @@ def _manifest():
 
 
 @pytest.mark.parametrize("spec", _manifest(), ids=lambda s: s["name"])
-@pytest.mark.parametrize("opt", [{}, {"disable_tiles": 1}, {"num_sms": 4, "min_chunk_keys": 64}])
+@pytest.mark.parametrize("opt", [{}, {"disable_tiles": 1}, {"num_sms": 4, "min_chunk_keys": 64},
+                                 {"kernel_variant": 1}])
 def test_plan_bit_exact_golden_cases(spec, opt):
     a = C.make_packed(spec)
     _compare(a, spec["Hq"], spec["Hkv"], spec["d"], spec["dv"], spec["dtype"], **opt)
 
 
+@pytest.mark.parametrize("variant", [0, 1])
 @pytest.mark.parametrize("name", ["c1", "c2", "c3", "c4", "c5"])
-def test_plan_bit_exact_bench_configs(name):
+def test_plan_bit_exact_bench_configs(name, variant):
     s = W.config(name)
-    got = _compare(W.offsets(s), s.Hq, s.Hkv, s.d, s.dv, s.dtype)
+    got = _compare(W.offsets(s), s.Hq, s.Hkv, s.d, s.dv, s.dtype, kernel_variant=variant)
     assert got["items"].shape[0] > 0
 
 
@@ -84,7 +88,8 @@ def test_plan_bit_exact_random_property():
         dt = str(rng.choice(["bf16", "f16", "f32"]))
         d = int(rng.choice([64, 128]))
         _compare(off, gqa * Hkv, Hkv, d, d, dt, num_sms=int(rng.choice([8, 148])),
-                 min_chunk_keys=int(rng.choice([64, 256])))
+                 min_chunk_keys=int(rng.choice([64, 256])),
+                 kernel_variant=int(rng.choice([0, 1])))
 
 
 def test_plan_invariants_c3():
