@@ -50,8 +50,7 @@ struct alignas(16) Shared {
   int item_idx[2];
   float red[2][4][kR];  // per-warp partial row maxima (double-buffered by block parity) / sums
   // merge queue: softmax thread 0 appends the units this CTA completes, warps 6-7 merge them
-  int mq[64];
-  int mq_tail, mq_head, mq_done, mq_closed, mq_resv;
+  dev::MergeQueue mq;
 };
 
 __device__ __forceinline__ void init_barriers(Shared* s) {
@@ -69,45 +68,17 @@ __device__ __forceinline__ void init_barriers(Shared* s) {
   dev::mbar_init(&s->s_full, 1);
   dev::mbar_init(&s->s_free, 4);
   dev::mbar_init(&s->o_done, 1);
-  s->mq_tail = s->mq_head = s->mq_done = s->mq_closed = s->mq_resv = 0;
+  dev::mq_init(&s->mq);
   dev::fence_mbar_init();
 }
 
-__device__ __forceinline__ int ld_volatile(const int* p) { return *reinterpret_cast<const volatile int*>(p); }
-__device__ __forceinline__ void st_volatile(int* p, int v) { *reinterpret_cast<volatile int*>(p) = v; }
-
-// Softmax threads: hand unit u to the merge warps (bounded ring; spins only if 64 are pending).
-// Slots are reserved with an atomic and published in order through mq_tail.
-__device__ __forceinline__ void enqueue_merge(Shared* sh, int u) {
-  const int slot = atomicAdd(&sh->mq_resv, 1);
-  while (slot - ld_volatile(&sh->mq_done) >= 64) __nanosleep(64);
-  st_volatile(&sh->mq[slot & 63], u);
-  __threadfence_block();
-  while (ld_volatile(&sh->mq_tail) != slot) __nanosleep(32);  // publish in slot order
-  st_volatile(&sh->mq_tail, slot + 1);
-}
+// Softmax threads: hand unit u to the merge warps (warps 6-7 of the pipeline).
+__device__ __forceinline__ void enqueue_merge(Shared* sh, int u) { dev::mq_push(&sh->mq, u); }
 
 // Warps 6-7: merge queued units until the queue is closed and drained.
 template <typename MergeUnit>
 __device__ __forceinline__ void merge_loop(Shared* sh, MergeUnit&& merge_unit) {
-  const int lane = threadIdx.x & 31;
-  for (;;) {
-    int u = -1;
-    if (lane == 0) {
-      const int h = atomicAdd(&sh->mq_head, 1);
-      for (;;) {
-        if (h < ld_volatile(&sh->mq_tail)) { u = ld_volatile(&sh->mq[h & 63]); break; }
-        if (ld_volatile(&sh->mq_closed) && h >= ld_volatile(&sh->mq_tail)) break;
-        __nanosleep(128);
-      }
-    }
-    u = __shfl_sync(0xffffffffu, u, 0);
-    if (u < 0) break;
-    __threadfence();  // acquire: the unit's partials were published before it was queued
-    merge_unit(u);
-    __syncwarp();
-    if (lane == 0) atomicAdd(&sh->mq_done, 1);
-  }
+  dev::mq_drain(&sh->mq, 1, merge_unit);
 }
 
 // Diagnostics: clock64 of per-block events of CTA 0's first 64 decode blocks, after
@@ -272,7 +243,13 @@ __device__ void run(const KParams& p, uint8_t* smem_raw, Shared* sh, uint32_t tm
           if (nb_s > 0) {
             const uint32_t cK = 2 * gS, s = cK % NSL;
             const bool sfree = gS == 0 || dev::mbar_test(&sh->s_free, (gS - 1) & 1);
-            if (sfree && dev::mbar_test(&sh->slot_full[s], (cK / NSL) & 1)) {
+            // A parity test tells phase o from phase o - 2 only once phase o - 1 has
+            // completed. With an odd ring, K_g's slot previously held V_j (cK - NSL =
+            // 2j + 1), which only the PV stream waits for: require PV_j issued (so V_j
+            // landed), else K_g's test could pass on phase o - 2 while V_j is in flight.
+            const int32_t prev = int32_t(cK) - int32_t(NSL);
+            const bool prev_ok = prev < 0 || !(prev & 1) || gP > uint32_t((prev - 1) >> 1);
+            if (sfree && prev_ok && dev::mbar_test(&sh->slot_full[s], (cK / NSL) & 1)) {
               dev::tc_fence_after();
               dbg(p, 2, gS);
               const uint32_t a0 = dev::smem_u32(G.slot(s)), b0 = dev::smem_u32(G.q(q));
@@ -342,10 +319,7 @@ __device__ void run(const KParams& p, uint8_t* smem_raw, Shared* sh, uint32_t tm
       dev::mbar_wait(&sh->item_full[q], (k >> 1) & 1);
       const int idx = sh->item_idx[q];
       if (idx < 0) {
-        if (t == 0) {
-          __threadfence_block();
-          st_volatile(&sh->mq_closed, 1);
-        }
+        if (t == 0) dev::mq_close(&sh->mq);
         break;
       }
       long long t_item0 = 0;

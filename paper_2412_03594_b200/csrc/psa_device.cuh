@@ -221,5 +221,77 @@ __host__ __device__ constexpr uint32_t umma_idesc_f16(uint32_t ab_format, uint32
          | ((M >> 4) << 24);       // m_dim
 }
 
+
+// ---- CTA-local merge queue ------------------------------------------------------
+// Bounded MPMC ring in shared memory: threads that complete a merge unit push it,
+// merge warps pop it. Every slot carries a sequence number (Vyukov): slot i is
+// free for ticket t when seq[i] == t, holds ticket t's unit when seq[i] == t + 1,
+// and is released for ticket t + kCap by the reader. A writer therefore never
+// overwrites an entry that has not been read, and a reader never sees an entry
+// before it is written, regardless of the order in which tickets complete.
+struct MergeQueue {
+  static constexpr int kCap = 64;
+  int unit[kCap];
+  int seq[kCap];
+  int resv;    // tickets handed to writers
+  int head;    // tickets handed to readers
+  int closed;  // producers that will not push again
+};
+
+__device__ __forceinline__ int ld_vol(const int* p) { return *reinterpret_cast<const volatile int*>(p); }
+__device__ __forceinline__ void st_vol(int* p, int v) { *reinterpret_cast<volatile int*>(p) = v; }
+
+// One thread.
+__device__ __forceinline__ void mq_init(MergeQueue* q) {
+  for (int i = 0; i < MergeQueue::kCap; ++i) q->seq[i] = i;
+  q->resv = q->head = q->closed = 0;
+}
+
+// Any thread: hand unit u to the merge warps (spins only while kCap units are pending).
+__device__ __forceinline__ void mq_push(MergeQueue* q, int u) {
+  const int t = atomicAdd(&q->resv, 1);
+  const int i = t & (MergeQueue::kCap - 1);
+  while (ld_vol(&q->seq[i]) != t) __nanosleep(32);
+  st_vol(&q->unit[i], u);
+  __threadfence_block();
+  st_vol(&q->seq[i], t + 1);
+}
+
+// One producer (thread) is done pushing; its pushes precede this in program order
+// (or are ordered before it by a barrier).
+__device__ __forceinline__ void mq_close(MergeQueue* q) {
+  __threadfence_block();
+  atomicAdd(&q->closed, 1);
+}
+
+// Merge warp: pop units until `closers` producers closed the queue and it is drained.
+template <typename MergeUnit>
+__device__ __forceinline__ void mq_drain(MergeQueue* q, int closers, MergeUnit&& merge_unit) {
+  const int lane = threadIdx.x & 31;
+  for (;;) {
+    int u = -1;
+    if (lane == 0) {
+      const int t = atomicAdd(&q->head, 1);
+      const int i = t & (MergeQueue::kCap - 1);
+      for (;;) {
+        if (ld_vol(&q->seq[i]) == t + 1) {
+          u = ld_vol(&q->unit[i]);
+          __threadfence_block();
+          st_vol(&q->seq[i], t + MergeQueue::kCap);
+          break;
+        }
+        // closed: every push is reserved; a ticket beyond them will never be filled
+        if (ld_vol(&q->closed) >= closers && t >= ld_vol(&q->resv)) break;
+        __nanosleep(64);
+      }
+    }
+    u = __shfl_sync(0xffffffffu, u, 0);
+    if (u < 0) break;
+    __threadfence();  // acquire: the unit's partials were published before it was queued
+    merge_unit(u);
+    __syncwarp();
+  }
+}
+
 }  // namespace dev
 }  // namespace psa

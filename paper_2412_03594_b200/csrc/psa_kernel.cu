@@ -930,7 +930,7 @@ __global__ void __launch_bounds__(kV2Threads, 1) psa_v2(const __grid_constant__ 
       setmaxnreg_dec_128();
     } else {
       setmaxnreg_dec_72();
-      if (warp >= tile2::kMergeWarp0) tile2::mq_loop(&s_t2.mq, 2, merge_u);
+      if (warp >= tile2::kMergeWarp0) dev::mq_drain(&s_t2.mq, 2, merge_u);
       else tile2::run_support<T>(p, smem, &s_t2, tmem, load_at);
       setmaxnreg_inc_128();
     }
@@ -938,7 +938,7 @@ __global__ void __launch_bounds__(kV2Threads, 1) psa_v2(const __grid_constant__ 
     __syncthreads();
     dev::tc_fence_after();
   }
-  if (p.use_dec) {
+  if (p.use_dec && (warp >> 3) < p.dec_pipes) {
     const int pi = warp >> 3;
     const size_t half = dec::pipe_stride(p.dec_slots);
     auto finish = [&](const ItemRec& it, int t, int R, const float (&m)[dec::kR],
@@ -1068,6 +1068,11 @@ int launch_v2(const KParams& p_in, int32_t num_sms, void* stream) {
   p.dec_slots = 2;
   while (p.dec_slots < dec::kMaxSlots && 2 * dec::pipe_stride(p.dec_slots + 1) <= budget)
     ++p.dec_slots;
+  // Diagnostics (PSA_DEBUG bit mask): 1 = one decode pipeline per CTA, 2 = two ring slots.
+  const char* dbg_env = std::getenv("PSA_DEBUG");
+  const int dbg = dbg_env ? std::atoi(dbg_env) : 0;
+  p.dec_pipes = (dbg & 1) ? 1 : 2;
+  if (dbg & 2) p.dec_slots = 2;
   size_t smem = 0;
   if (p.use_tiles) smem = tile2::smem_bytes(p.tile_stages);
   if (p.use_dec) {

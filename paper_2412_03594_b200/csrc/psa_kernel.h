@@ -67,6 +67,7 @@ struct KParams {
   int32_t tile_stages;   // TILE K/V ring depth (set by the launcher from the smem budget)
   int32_t dec_slots;     // decode K/V ring slots (ditto)
   int32_t use_v2;       // v2 kernel: 1 CTA/SM, paired tile slots + two decode pipelines
+  int32_t dec_pipes;    // v2: decode pipelines per CTA (2; 1 under PSA_DEBUG bit 0)
   double scale;
   int64_t* trace;        // diagnostics: per item {cta | smid << 32, kind, t_start, t_end}
 };

@@ -49,20 +49,13 @@ constexpr float kRescaleThreshold = 8.0f;  // log2 units
 constexpr int kProducerWarp = 8, kMmaWarp = 9, kMergeWarp0 = 10;
 constexpr int kThreads = 512;
 
-// CTA-local merge queue: softmax threads append units whose last contribution
-// they delivered; merge warps drain it.
-struct MergeQ {
-  int mq[64];
-  int tail, head, done, closed, resv;
-};
-
 struct Shared {
   uint64_t item_full[2], item_empty[2];
   uint64_t q_full, q_empty;
   uint64_t ring_full[kMaxRing], ring_empty[kMaxRing];
   uint64_t s_full[2], p_full[2], o_full[2], o_empty[2];
   int item_idx[2];
-  MergeQ mq;
+  dev::MergeQueue mq;
 };
 
 __host__ __device__ constexpr size_t smem_bytes(int ring) {
@@ -84,43 +77,8 @@ __device__ __forceinline__ void init(Shared* s) {
     dev::mbar_init(&s->ring_full[i], 1);
     dev::mbar_init(&s->ring_empty[i], 1);
   }
-  s->mq.tail = s->mq.head = s->mq.done = s->mq.closed = s->mq.resv = 0;
+  dev::mq_init(&s->mq);
   dev::fence_mbar_init();
-}
-
-__device__ __forceinline__ int ld_volatile(const int* p) { return *reinterpret_cast<const volatile int*>(p); }
-__device__ __forceinline__ void st_volatile(int* p, int v) { *reinterpret_cast<volatile int*>(p) = v; }
-
-__device__ __forceinline__ void mq_push(MergeQ* q, int u) {
-  const int slot = atomicAdd(&q->resv, 1);
-  while (slot - ld_volatile(&q->done) >= 64) __nanosleep(64);
-  st_volatile(&q->mq[slot & 63], u);
-  __threadfence_block();
-  while (ld_volatile(&q->tail) != slot) __nanosleep(32);  // publish in slot order
-  st_volatile(&q->tail, slot + 1);
-}
-
-// Merge warps: drain until `closers` producers closed the queue and it is empty.
-template <typename MergeUnit>
-__device__ __forceinline__ void mq_loop(MergeQ* q, int closers, MergeUnit&& merge_unit) {
-  const int lane = threadIdx.x & 31;
-  for (;;) {
-    int u = -1;
-    if (lane == 0) {
-      const int h = atomicAdd(&q->head, 1);
-      for (;;) {
-        if (h < ld_volatile(&q->tail)) { u = ld_volatile(&q->mq[h & 63]); break; }
-        if (ld_volatile(&q->closed) >= closers && h >= ld_volatile(&q->tail)) break;
-        __nanosleep(128);
-      }
-    }
-    u = __shfl_sync(0xffffffffu, u, 0);
-    if (u < 0) break;
-    __threadfence();  // acquire: the unit's partials were published before it was queued
-    merge_unit(u);
-    __syncwarp();
-    if (lane == 0) atomicAdd(&q->done, 1);
-  }
 }
 
 struct Geo {
@@ -556,7 +514,7 @@ __device__ void run_softmax(const KParams& p, Shared* sh, uint32_t tmem, LoadIte
           const int need = __ldg(U + (int64_t)u * kUnitWords + kUnContribCount);
           if (atomicAdd(p.unit_cnt + u, 1) == need - 1) {
             p.unit_cnt[u] = 0;
-            mq_push(&sh->mq, u);
+            dev::mq_push(&sh->mq, u);
           }
         }
       } else {
@@ -608,10 +566,7 @@ __device__ void run_softmax(const KParams& p, Shared* sh, uint32_t tmem, LoadIte
     }
     // this WG will not queue more merges
     named_sync(2 + i, 128);
-    if ((threadIdx.x & 127) == 0) {
-      __threadfence_block();
-      atomicAdd(&sh->mq.closed, 1);
-    }
+    if ((threadIdx.x & 127) == 0) dev::mq_close(&sh->mq);
   }
 }
 

@@ -77,6 +77,29 @@ def test_repeat_launches_are_bit_identical_and_reset_counters():
     assert ctrl[0].item() == 0 and ctrl[1].item() == 0
 
 
+@pytest.mark.parametrize("opts", [dict(), dict(disable_tiles=1), dict(kernel_variant=1),
+                                  dict(kernel_variant=1, disable_tiles=1)],
+                         ids=["v2", "v2_dec_only", "v1", "v1_dec_only"])
+def test_skewed_batch_many_launches_bit_identical(opts):
+    """c4 (skewed groups) relaunched many times: every launch must be bitwise equal.
+    Catches pipeline phase races (e.g. a ring slot consumed one phase early), which
+    show up as rare single-token differences or a faulting mbarrier."""
+    spec = W.config("c4")
+    b = W.make_batch(spec, "cuda")
+    op = P.PrefixSharedAttention(b["cu_req"], b["cu_q"], b["cu_prefix"], b["cu_distinct"],
+                                 spec.Hq, spec.Hkv, spec.d, spec.dv, spec.torch_dtype, "cuda",
+                                 options=P.PlanOptions(**opts))
+    keys = ("q", "k_prefix", "v_prefix", "k_distinct", "v_distinct")
+    ref = op(*(b[k] for k in keys)).clone()
+    out = torch.empty_like(ref)
+    for i in range(60):
+        op(*(b[k] for k in keys), out=out)
+        torch.cuda.synchronize()
+        assert torch.equal(out, ref), f"launch {i + 1} differs from launch 0"
+    assert op.device_error() == 0
+    check_sampled_groups(spec, b, ref, n_groups=2, n_heads=1)
+
+
 @pytest.mark.parametrize("name", ["c2", "c4"])
 def test_relaunch_with_new_inputs_recomputes_everything(name):
     """One planned op, several launches with different inputs (and a poisoned
