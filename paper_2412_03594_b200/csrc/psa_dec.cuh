@@ -72,10 +72,11 @@ __device__ __forceinline__ void init_barriers(Shared* s) {
   dev::fence_mbar_init();
 }
 
-// Softmax threads: hand unit u to the merge warps (warps 6-7 of the pipeline).
-__device__ __forceinline__ void enqueue_merge(Shared* sh, int u) { dev::mq_push(&sh->mq, u); }
+// Softmax thread 0: hand an item whose partial rows are stored (and ordered before
+// this by a named barrier) to the merge warps (warps 6-7 of the pipeline).
+__device__ __forceinline__ void enqueue_merge(Shared* sh, int idx) { dev::mq_push(&sh->mq, idx); }
 
-// Warps 6-7: merge queued units until the queue is closed and drained.
+// Warps 6-7: arrive at / merge the queued items' units until the queue is closed and drained.
 template <typename MergeUnit>
 __device__ __forceinline__ void merge_loop(Shared* sh, MergeUnit&& merge_unit) {
   dev::mq_drain(&sh->mq, 1, merge_unit);
@@ -452,7 +453,7 @@ __device__ void run(const KParams& p, uint8_t* smem_raw, Shared* sh, uint32_t tm
       float ov[kR];
 #pragma unroll
       for (int r = 0; r < kR; ++r) ov[r] = __uint_as_float(o[r]);
-      finish(it, t, R, m, L, ov);  // writes output / partial, arrives at merge units
+      finish(it, idx, t, R, m, L, ov);  // output, or partial rows queued for arrival
       if (t == 0) dbg(p, 9, g - 1);
       named_sync_softmax(pi);      // red[] reuse + item slot release after everyone finished
       if (t == 0) dev::mbar_arrive(&sh->item_empty[q]);

@@ -223,19 +223,22 @@ __host__ __device__ constexpr uint32_t umma_idesc_f16(uint32_t ab_format, uint32
 
 
 // ---- CTA-local merge queue ------------------------------------------------------
-// Bounded MPMC ring in shared memory: threads that complete a merge unit push it,
-// merge warps pop it. Every slot carries a sequence number (Vyukov): slot i is
-// free for ticket t when seq[i] == t, holds ticket t's unit when seq[i] == t + 1,
-// and is released for ticket t + kCap by the reader. A writer therefore never
-// overwrites an entry that has not been read, and a reader never sees an entry
-// before it is written, regardless of the order in which tickets complete.
+// Bounded MPMC ring in shared memory: threads that complete work push tasks, merge
+// warps pop them (and may push follow-up tasks). Every slot carries a sequence
+// number (Vyukov): slot i is free for ticket t when seq[i] == t, holds ticket t's
+// task when seq[i] == t + 1, and is released for ticket t + kCap by the reader, so
+// a writer never overwrites an unread entry and a reader never sees an unwritten one.
+// Termination: `outstanding` counts tasks pushed and not yet finished (a task's
+// follow-up pushes happen before it finishes); readers leave once every producer
+// closed and nothing is outstanding.
 struct MergeQueue {
   static constexpr int kCap = 64;
   int unit[kCap];
   int seq[kCap];
-  int resv;    // tickets handed to writers
-  int head;    // tickets handed to readers
-  int closed;  // producers that will not push again
+  int resv;         // tickets handed to writers
+  int head;         // tickets handed to readers
+  int closed;       // producers that will not push again
+  int outstanding;  // tasks pushed and not yet finished
 };
 
 __device__ __forceinline__ int ld_vol(const int* p) { return *reinterpret_cast<const volatile int*>(p); }
@@ -244,11 +247,12 @@ __device__ __forceinline__ void st_vol(int* p, int v) { *reinterpret_cast<volati
 // One thread.
 __device__ __forceinline__ void mq_init(MergeQueue* q) {
   for (int i = 0; i < MergeQueue::kCap; ++i) q->seq[i] = i;
-  q->resv = q->head = q->closed = 0;
+  q->resv = q->head = q->closed = q->outstanding = 0;
 }
 
-// Any thread: hand unit u to the merge warps (spins only while kCap units are pending).
+// Any thread: hand task u to the merge warps (spins only while kCap tasks are pending).
 __device__ __forceinline__ void mq_push(MergeQueue* q, int u) {
+  atomicAdd(&q->outstanding, 1);
   const int t = atomicAdd(&q->resv, 1);
   const int i = t & (MergeQueue::kCap - 1);
   while (ld_vol(&q->seq[i]) != t) __nanosleep(32);
@@ -264,32 +268,48 @@ __device__ __forceinline__ void mq_close(MergeQueue* q) {
   atomicAdd(&q->closed, 1);
 }
 
-// Merge warp: pop units until `closers` producers closed the queue and it is drained.
-template <typename MergeUnit>
-__device__ __forceinline__ void mq_drain(MergeQueue* q, int closers, MergeUnit&& merge_unit) {
+// Tasks pushed and not yet claimed by a reader (negative while readers wait). A
+// pusher that sees fewer than kCap / 2 pending can push without blocking as long
+// as at most kCap / 4 pushers race (each waiting reader holds at most one slot).
+__device__ __forceinline__ int mq_pending(const MergeQueue* q) {
+  return ld_vol(&q->resv) - ld_vol(&q->head);
+}
+
+// Merge warp: pop tasks until `closers` producers closed the queue and no task is
+// outstanding.
+template <typename Task>
+__device__ __forceinline__ void mq_drain(MergeQueue* q, int closers, Task&& task) {
   const int lane = threadIdx.x & 31;
   for (;;) {
-    int u = -1;
+    int u = 0, ok = 0;
     if (lane == 0) {
       const int t = atomicAdd(&q->head, 1);
       const int i = t & (MergeQueue::kCap - 1);
       for (;;) {
         if (ld_vol(&q->seq[i]) == t + 1) {
           u = ld_vol(&q->unit[i]);
+          ok = 1;
           __threadfence_block();
           st_vol(&q->seq[i], t + MergeQueue::kCap);
           break;
         }
-        // closed: every push is reserved; a ticket beyond them will never be filled
-        if (ld_vol(&q->closed) >= closers && t >= ld_vol(&q->resv)) break;
+        if (ld_vol(&q->closed) >= closers) {
+          __threadfence_block();
+          if (ld_vol(&q->outstanding) == 0) break;
+        }
         __nanosleep(64);
       }
     }
+    ok = __shfl_sync(0xffffffffu, ok, 0);
+    if (!ok) break;
     u = __shfl_sync(0xffffffffu, u, 0);
-    if (u < 0) break;
-    __threadfence();  // acquire: the unit's partials were published before it was queued
-    merge_unit(u);
+    __threadfence();  // acquire: the task's partial rows were published before it was queued
+    task(u);
     __syncwarp();
+    if (lane == 0) {
+      __threadfence_block();
+      atomicSub(&q->outstanding, 1);
+    }
   }
 }
 

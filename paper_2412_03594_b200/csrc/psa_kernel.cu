@@ -20,6 +20,7 @@
 
 #include <algorithm>
 #include <cfloat>
+#include <climits>
 #include <cmath>
 #include <cstdint>
 #include <cstring>
@@ -664,11 +665,47 @@ __device__ __forceinline__ void warp_arrive_and_merge(const KParams& p, const It
   }
 }
 
+// Merge-warp arrival on behalf of an item whose partial rows [r0, r1) (group rows)
+// were published to this warp through the CTA merge queue: one fence (cumulative
+// over the queue handoff), one atomic per unit whose first row lies in the range;
+// `on_last(u)` gets every unit this arrival completed (merge it now, or queue it so
+// several merge warps share a tile's units). Keeps the gpu-scope fence and the
+// merges off the softmax warps' critical path.
+template <typename OnLast>
+__device__ __forceinline__ void warp_arrive_rows(const KParams& p, const ItemRec& it, int r0,
+                                                 int r1, OnLast&& on_last) {
+  const int lane = threadIdx.x & 31;
+  __threadfence();
+  __syncwarp();
+  for (int base = it.u0; base < it.u1; base += 32) {
+    const int u = base + lane;
+    bool is_last = false;
+    if (u < it.u1) {
+      const int32_t* U = p.units + (int64_t)u * kUnitWords;
+      const int ur0 = __ldg(U + kUnRow0);
+      if (ur0 >= r0 && ur0 < r1) {
+        const int need = __ldg(U + kUnContribCount);
+        if (atomicAdd(p.unit_cnt + u, 1) == need - 1) {
+          p.unit_cnt[u] = 0;
+          is_last = true;
+        }
+      }
+    }
+    uint32_t last = __ballot_sync(0xffffffffu, is_last);
+    if (last) __threadfence();  // acquire: the other contributors' partial rows
+    while (last) {
+      const int bit = __ffs(last) - 1;
+      last &= last - 1;
+      on_last(base + bit);
+    }
+  }
+}
+
 // End of a decode item (thread t = value column t of the item's <= 8 rows): the
 // partial rows + arrival at the merge units, or the final output.
 template <typename T>
 __device__ __forceinline__ void dec_finish(const KParams& p, dec::Shared* sh, const ItemRec& it,
-                                           int t, int R, const float (&m)[dec::kR],
+                                           int idx, int t, int R, const float (&m)[dec::kR],
                                            const float (&L)[dec::kR], const float (&ov)[dec::kR],
                                            int pi) {
   if (it.ws_row >= 0) {
@@ -683,17 +720,9 @@ __device__ __forceinline__ void dec_finish(const KParams& p, dec::Shared* sh, co
           *reinterpret_cast<float2*>(static_cast<float*>(p.ws_ml) + ((int64_t)it.ws_row + r) * 2) =
               make_float2(m[r], L[r]);
     }
+    // publish to the pipeline's merge warps, which arrive at the item's units
     dec::named_sync_softmax(pi);
-    const int nu = it.u1 - it.u0;  // <= 9 units: one thread each
-    if (t < nu) {
-      const int u = it.u0 + t;
-      __threadfence();  // release: this item's partial rows (cumulative over the barrier)
-      const int need = __ldg(p.units + (int64_t)u * kUnitWords + kUnContribCount);
-      if (atomicAdd(p.unit_cnt + u, 1) == need - 1) {
-        p.unit_cnt[u] = 0;
-        dec::enqueue_merge(sh, u);
-      }
-    }
+    if (t == 0) dec::enqueue_merge(sh, idx);
     return;
   }
   const int64_t tok0 = __ldg(p.group_tok0 + it.g);
@@ -832,12 +861,15 @@ __global__ void __launch_bounds__(kThreads, 2) psa_persistent(const __grid_const
     };
     auto dec_phase = [&]() {
       auto load_at = [&](int idx) { return load_item(p.items + (int64_t)idx * kItemWords); };
-      auto finish = [&](const ItemRec& it, int t, int R, const float (&m)[dec::kR],
+      auto finish = [&](const ItemRec& it, int idx, int t, int R, const float (&m)[dec::kR],
                         const float (&L)[dec::kR], const float (&ov)[dec::kR]) {
-        dec_finish<T>(p, &s_dec, it, t, R, m, L, ov, 0);
+        dec_finish<T>(p, &s_dec, it, idx, t, R, m, L, ov, 0);
       };
-      auto merge_u = [&](int u) { merge_unit_warp<T>(p, u); };
-      dec::run<T>(p, smem, &s_dec, tst.tmem, 0, load_at, finish, merge_u);
+      auto arrive = [&](int idx) {
+        warp_arrive_rows(p, load_at(idx), INT_MIN, INT_MAX,
+                         [&](int u) { merge_unit_warp<T>(p, u); });
+      };
+      dec::run<T>(p, smem, &s_dec, tst.tmem, 0, load_at, finish, arrive);
     };
     if (dec_on) {
       cta_phase(p.n_tile_items);
@@ -893,7 +925,7 @@ __device__ __forceinline__ void setmaxnreg_dec_72() { asm volatile("setmaxnreg.d
 __device__ __forceinline__ void setmaxnreg_dec_128() { asm volatile("setmaxnreg.dec.sync.aligned.u32 128;"); }
 __device__ __forceinline__ void setmaxnreg_inc_128() { asm volatile("setmaxnreg.inc.sync.aligned.u32 128;"); }
 
-template <typename T>
+template <typename T, int kEmu>
 __global__ void __launch_bounds__(kV2Threads, 1) psa_v2(const __grid_constant__ KParams p) {
   extern __shared__ __align__(1024) uint8_t smem[];
   __shared__ tile2::Shared s_t2;
@@ -921,32 +953,71 @@ __global__ void __launch_bounds__(kV2Threads, 1) psa_v2(const __grid_constant__ 
   dev::tc_fence_after();
   const uint32_t tmem = s_tmem;
   auto load_at = [&](int idx) { return load_item(p.items + (int64_t)idx * kItemWords); };
-  auto merge_u = [&](int u) { merge_unit_warp<T>(p, u); };
+  // Merge-queue tasks. Decode pipelines: an item index (arrive at all its units,
+  // merge the completed ones). Tile phase: 2 * item + slot (arrive at the units of
+  // that slot's rows) or ~u (merge unit u): a slot can complete dozens of units, so
+  // they go back to the queue and all six merge warps share them.
+  auto merge_now = [&](int u) { merge_unit_warp<T>(p, u); };
+  auto arrive_dec = [&](int idx) { warp_arrive_rows(p, load_at(idx), INT_MIN, INT_MAX, merge_now); };
+  auto tile_task = [&](int task) {
+    if (task < 0) {
+      merge_unit_warp<T>(p, ~task);
+      return;
+    }
+    const ItemRec it = load_at(task >> 1);
+    const int tile_rows = p.gqa * (tile2::kM / p.gqa);
+    const int i = task & 1;
+    const int r0 = it.row0 + i * tile_rows;
+    const int r1 = i == 0 ? it.row0 + min(it.nrows, tile_rows) : it.row0 + it.nrows;
+    warp_arrive_rows(p, it, r0, r1, [&](int u) {
+      int queued = 0;
+      if ((threadIdx.x & 31) == 0 && dev::mq_pending(&s_t2.mq) < dev::MergeQueue::kCap / 2) {
+        dev::mq_push(&s_t2.mq, ~u);
+        queued = 1;
+      }
+      if (!__shfl_sync(0xffffffffu, queued, 0)) merge_unit_warp<T>(p, u);
+    });
+  };
 
+  // diagnostics: per-CTA phase record {t(softmax done), t(producer/MMA done), t(merge
+  // warps done), t(tile phase barrier passed)} at trace row num_items + 2048 + CTA
+  auto phase_mark = [&](int field) {
+    if (p.trace_cap > 0 && (threadIdx.x & 31) == 0)
+      atomicMax(reinterpret_cast<unsigned long long*>(
+                    p.trace + (int64_t(p.num_items) + 2048 + blockIdx.x) * 4 + field),
+                (unsigned long long)globaltimer());
+  };
   if (p.use_tiles) {
     if (warp < 8) {
       setmaxnreg_inc_184();
-      tile2::run_softmax<T, kV2EmuEvery>(p, &s_t2, tmem, load_at);
+      tile2::run_softmax<T, kEmu>(p, &s_t2, tmem, load_at);
+      phase_mark(0);
       setmaxnreg_dec_128();
     } else {
       setmaxnreg_dec_72();
-      if (warp >= tile2::kMergeWarp0) dev::mq_drain(&s_t2.mq, 2, merge_u);
-      else tile2::run_support<T>(p, smem, &s_t2, tmem, load_at);
+      if (warp >= tile2::kMergeWarp0) {
+        dev::mq_drain(&s_t2.mq, 2, tile_task);
+        phase_mark(2);
+      } else {
+        tile2::run_support<T>(p, smem, &s_t2, tmem, load_at);
+        phase_mark(1);
+      }
       setmaxnreg_inc_128();
     }
     dev::tc_fence_before();
     __syncthreads();
     dev::tc_fence_after();
+    if (threadIdx.x == 0) phase_mark(3);
   }
   if (p.use_dec && (warp >> 3) < p.dec_pipes) {
     const int pi = warp >> 3;
     const size_t half = dec::pipe_stride(p.dec_slots);
-    auto finish = [&](const ItemRec& it, int t, int R, const float (&m)[dec::kR],
+    auto finish = [&](const ItemRec& it, int idx, int t, int R, const float (&m)[dec::kR],
                       const float (&L)[dec::kR], const float (&ov)[dec::kR]) {
-      dec_finish<T>(p, &s_dec[pi], it, t, R, m, L, ov, pi);
+      dec_finish<T>(p, &s_dec[pi], it, idx, t, R, m, L, ov, pi);
     };
     dec::run<T>(p, smem + pi * half, &s_dec[pi], tmem + 64u * uint32_t(pi), pi, load_at, finish,
-                merge_u);
+                arrive_dec);
   }
   __syncthreads();
   if (p.trace_cap > 0 && threadIdx.x == 0) trace_item(p, p.num_items + int(blockIdx.x), -1, t_kernel0);
@@ -1078,10 +1149,13 @@ int launch_v2(const KParams& p_in, int32_t num_sms, void* stream) {
   if (p.use_dec) {
     smem = std::max(smem, 2 * dec::pipe_stride(p.dec_slots));
   }
-  cudaError_t e = cudaFuncSetAttribute(psa_v2<T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  // PSA_DEBUG bits 2-3 (diagnostics): tile softmax exp emulation every 2nd / 3rd pair
+  auto kern = psa_v2<T, kV2EmuEvery>;
+  if ((dbg >> 2) & 3) kern = ((dbg >> 2) & 3) == 1 ? psa_v2<T, 2> : ((dbg >> 2) & 3) == 2 ? psa_v2<T, 3> : psa_v2<T, 0>;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        int(smem));
   if (e != cudaSuccess) return e;
-  psa_v2<T><<<num_sms, kV2Threads, smem, static_cast<cudaStream_t>(stream)>>>(p);
+  kern<<<num_sms, kV2Threads, smem, static_cast<cudaStream_t>(stream)>>>(p);
   return cudaGetLastError();
 }
 

@@ -133,35 +133,47 @@ __device__ __forceinline__ void fadd2(float& s0, float& s1, float a0, float a1) 
   s1 = __uint_as_float(uint32_t(r >> 32));
 }
 
-// 2^x for x <= 0 on the FMA pipe (two lanes): clamp to -127, x = j + f with
+// Packed fp32x2 helpers with per-lane operands.
+__device__ __forceinline__ uint64_t pk(float a0, float a1) {
+  return (uint64_t(__float_as_uint(a1)) << 32) | __float_as_uint(a0);
+}
+__device__ __forceinline__ uint64_t fma2v(uint64_t a, uint64_t b, uint64_t c) {
+  uint64_t r;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(a), "l"(b), "l"(c));
+  return r;
+}
+__device__ __forceinline__ uint64_t add2v(uint64_t a, uint64_t b) {
+  uint64_t r;
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+  return r;
+}
+
+// 2^x for x <= 0 on the FMA pipe (two lanes): clamp to -126, x = j + f with
 // j = round(x) (magic-number add), f in [-0.5, 0.5]; 2^f by a cubic
-// (max rel. error 7.5e-5, far below the bf16 rounding of P), 2^j by an exponent add.
+// (max rel. error 7.5e-5, far below the bf16 rounding of P), 2^j by adding j to
+// the exponent field (t = x + 1.5 * 2^23 holds j in its low bits: t << 23 = j << 23).
 __device__ __forceinline__ void exp2_poly2(float& y0, float& y1, float x0, float x1) {
-  x0 = fmaxf(x0, -126.f);  // 2^j stays a (sub)normal exponent for j >= -126
-  x1 = fmaxf(x1, -126.f);
-  const float kMagic = 12582912.f;  // 1.5 * 2^23: t = x + kMagic holds round(x) in its low bits
-  float t0, t1, p0, p1;
-  ffma2(t0, t1, x0, x1, 1.f, kMagic);
-  float j0 = t0, j1 = t1;
-  fadd2(j0, j1, -kMagic, -kMagic);  // j = round(x)
-  float f0 = x0, f1 = x1;
-  fadd2(f0, f1, -j0, -j1);          // f = x - j in [-0.5, 0.5]
-  // minimax cubic for 2^f on [-0.5, 0.5]
+  const float kMagic = 12582912.f;  // 1.5 * 2^23
+  const uint64_t X = pk(fmaxf(x0, -126.f), fmaxf(x1, -126.f));
+  const uint64_t T = add2v(X, pk(kMagic, kMagic));            // t = x + magic
+  const uint64_t J = add2v(T, pk(-kMagic, -kMagic));          // j = round(x)
+  const uint64_t F = fma2v(J, pk(-1.f, -1.f), X);              // f = x - j
   const float c3 = 0.05517132f, c2 = 0.24261054f, c1 = 0.69326099f, c0 = 0.99992811f;
-  ffma2(p0, p1, f0, f1, c3, c2);
-  {
-    uint64_t r;
-    const uint64_t P = (uint64_t(__float_as_uint(p1)) << 32) | __float_as_uint(p0);
-    const uint64_t F = (uint64_t(__float_as_uint(f1)) << 32) | __float_as_uint(f0);
-    const uint64_t C1 = (uint64_t(__float_as_uint(c1)) << 32) | __float_as_uint(c1);
-    const uint64_t C0 = (uint64_t(__float_as_uint(c0)) << 32) | __float_as_uint(c0);
-    asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(P), "l"(F), "l"(C1));
-    asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(r), "l"(F), "l"(C0));
-    p0 = __uint_as_float(uint32_t(r));
-    p1 = __uint_as_float(uint32_t(r >> 32));
-  }
-  y0 = __uint_as_float(__float_as_uint(p0) + (__float_as_uint(t0) << 23));
-  y1 = __uint_as_float(__float_as_uint(p1) + (__float_as_uint(t1) << 23));
+  uint64_t P = fma2v(F, pk(c3, c3), pk(c2, c2));
+  P = fma2v(P, F, pk(c1, c1));
+  P = fma2v(P, F, pk(c0, c0));
+  uint32_t r0, r1;
+  asm("{\n\t.reg .b32 t0, t1, p0, p1;\n\t"
+      "mov.b64 {t0, t1}, %2;\n\t"
+      "mov.b64 {p0, p1}, %3;\n\t"
+      "shl.b32 t0, t0, 23;\n\t"
+      "shl.b32 t1, t1, 23;\n\t"
+      "add.u32 %0, p0, t0;\n\t"
+      "add.u32 %1, p1, t1;\n\t}"
+      : "=r"(r0), "=r"(r1)
+      : "l"(T), "l"(P));
+  y0 = __uint_as_float(r0);
+  y1 = __uint_as_float(r1);
 }
 
 struct Block {
@@ -197,6 +209,16 @@ __device__ __forceinline__ void item_shape(const KParams& p, const ItemT& it, in
   nb = nbA + (it.dk1 - it.dk0 + kBN - 1) / kBN;
   pbase = nbA ? __ldg(p.group_pbase + it.g) : 0;
   dbase = (it.dk1 > it.dk0 && it.req >= 0) ? __ldg(p.req_dbase + it.req) : 0;
+}
+
+// Diagnostics: clock64 of per-block events of CTA 0 (first 64 blocks), slot 0.
+// Slot = event * 64 + block, after the item records (psa_debug_set_trace).
+__device__ __forceinline__ void dbg(const KParams& p, int ev, uint32_t g) {
+  if (p.trace_cap > 0 && blockIdx.x == 0 && g < 64) {
+    long long t;
+    asm volatile("mov.u64 %0, %%clock64;" : "=l"(t));
+    p.trace[(int64_t(p.num_items) + 4096) * 4 + ev * 64 + g] = t;
+  }
 }
 
 __device__ __forceinline__ void named_sync(int id, int threads) {
@@ -262,6 +284,7 @@ __device__ void run_support(const KParams& p, uint8_t* smem_raw, Shared* sh, uin
             dev::mbar_wait(&sh->ring_empty[s], ((c / NR) & 1) ^ 1);
             dev::mbar_arrive_expect_tx(&sh->ring_full[s], kSlotBytes);
             const CUtensorMap* m = w == 0 ? b.km : b.vm;
+            dbg(p, 7 + w, c >> 1);
             dev::tma_load_3d(G.slot(s), m, &sh->ring_full[s], 0, it.h, b.key);
             dev::tma_load_3d(G.slot(s) + kBN * 128, m, &sh->ring_full[s], 64, it.h, b.key);
           }
@@ -328,8 +351,10 @@ __device__ void run_support(const KParams& p, uint8_t* smem_raw, Shared* sh, uin
               dev::mbar_wait(&sh->p_full[i], nblk[i] & 1);
               ++nblk[i];
               dev::tc_fence_after();
+              if (i == 0) dbg(p, 6, gb + n - 1);
               issue_pv(i, sV, n == 1);
             }
+            if (i == 0) dbg(p, 5, gb + n);
             issue_s(i, sK);
           }
           if (n > 0) dev::mma_commit(&sh->ring_empty[sV]);
@@ -376,6 +401,8 @@ __device__ void run_softmax(const KParams& p, Shared* sh, uint32_t tmem, LoadIte
       const int idx = sh->item_idx[q];
       if (idx < 0) break;
       const auto it = load_item_at(idx);
+      long long t_item0 = 0;
+      if (p.trace_cap > 0 && threadIdx.x == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_item0));
       named_sync(2 + i, 128);  // every thread of the WG has read item_idx[q]
       if (threadIdx.x % 128 == 0) dev::mbar_arrive(&sh->item_empty[q]);
       const int slot_rows = i == 0 ? min(it.nrows, tile_rows) : it.nrows - tile_rows;
@@ -388,6 +415,8 @@ __device__ void run_softmax(const KParams& p, Shared* sh, uint32_t tmem, LoadIte
         const int nvalid = n < nbA ? min(kBN, it.pk1 - it.pk0 - n * kBN)
                                    : min(kBN, it.dk1 - it.dk0 - (n - nbA) * kBN);
         dev::mbar_wait(&sh->s_full[i], nblk & 1);
+        const bool ev = threadIdx.x == 0;
+        if (ev) dbg(p, 0, nblk);
         dev::tc_fence_after();
         uint32_t r[4][32];
         dev::tmem_ld32(tS + 0, r[0]);
@@ -395,6 +424,7 @@ __device__ void run_softmax(const KParams& p, Shared* sh, uint32_t tmem, LoadIte
         dev::tmem_ld32(tS + 64, r[2]);
         dev::tmem_ld32(tS + 96, r[3]);
         dev::tmem_wait_ld();
+        if (ev) dbg(p, 1, nblk);
         if (nvalid < kBN) {
 #pragma unroll
           for (int c = 0; c < 4; ++c)
@@ -414,6 +444,7 @@ __device__ void run_softmax(const KParams& p, Shared* sh, uint32_t tmem, LoadIte
         }
         const float mraw = max3(max3(a8[0], a8[1], a8[2]), max3(a8[3], a8[4], a8[5]), fmaxf(a8[6], a8[7]));
         const float mb = mraw * sc;
+        if (ev) dbg(p, 2, nblk);
         float alpha = 1.f;
         bool rescale = false;
         if (m == -INFINITY) {
@@ -443,6 +474,7 @@ __device__ void run_softmax(const KParams& p, Shared* sh, uint32_t tmem, LoadIte
             r[c][e] = pack2<T>(y0, y1);
           }
         }
+        if (ev) dbg(p, 3, nblk);
         // P_n -> S_i columns [0, 64)
         {
           uint32_t hi[32];
@@ -471,6 +503,7 @@ __device__ void run_softmax(const KParams& p, Shared* sh, uint32_t tmem, LoadIte
         dev::tc_fence_before();
         __syncwarp();
         if (lane == 0) dev::mbar_arrive(&sh->p_full[i]);
+        if (ev) dbg(p, 4, nblk);
       }
       // ---------------- epilogue: O_i -> output / partial ----------------
       dev::mbar_wait(&sh->o_full[i], nitem & 1);
@@ -503,20 +536,10 @@ __device__ void run_softmax(const KParams& p, Shared* sh, uint32_t tmem, LoadIte
         if (valid)
           *reinterpret_cast<float2*>(static_cast<float*>(p.ws_ml) +
                                      ((int64_t)it.ws_row + i * tile_rows + row) * 2) = make_float2(m, l);
-        // publish the slot's partial rows, then arrive at the units they cover
+        // publish the slot's partial rows to the merge warps, which arrive at the
+        // units they cover (and merge or queue the units they complete)
         named_sync(2 + i, 128);
-        const int32_t* U = p.units;
-        const int r0 = slot_row0, r1 = slot_row0 + slot_rows;
-        for (int u = it.u0 + (threadIdx.x & 127); u < it.u1; u += 128) {
-          const int ur0 = __ldg(U + (int64_t)u * kUnitWords + kUnRow0);
-          if (ur0 < r0 || ur0 >= r1) continue;
-          __threadfence();
-          const int need = __ldg(U + (int64_t)u * kUnitWords + kUnContribCount);
-          if (atomicAdd(p.unit_cnt + u, 1) == need - 1) {
-            p.unit_cnt[u] = 0;
-            dev::mq_push(&sh->mq, u);
-          }
-        }
+        if ((threadIdx.x & 127) == 0) dev::mq_push(&sh->mq, 2 * idx + i);
       } else {
         const int grow = slot_row0 + row;
         const int64_t tok = __ldg(p.group_tok0 + it.g) + grow / gqa;
@@ -562,6 +585,17 @@ __device__ void run_softmax(const KParams& p, Shared* sh, uint32_t tmem, LoadIte
             if (p.lse) p.lse[oidx] = (m + log2f(l)) * 0.6931471805599453f;
           }
         }
+      }
+      if (p.trace_cap > 0 && threadIdx.x == 0 && idx < p.trace_cap) {  // diagnostics
+        long long t1;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1));
+        uint32_t smid;
+        asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+        int64_t* tr = p.trace + int64_t(idx) * 4;
+        tr[0] = int64_t(blockIdx.x) | (int64_t(smid) << 32);
+        tr[1] = 1;
+        tr[2] = t_item0;
+        tr[3] = t1;
       }
     }
     // this WG will not queue more merges

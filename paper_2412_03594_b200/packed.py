@@ -226,6 +226,7 @@ class PrefixSharedAttention:
         out = buf.cpu().numpy()
         self.last_tile_events = out[n:].reshape(-1)[:9 * 64].reshape(9, 64)
         self.last_dec_events = out[n:].reshape(-1)[16 * 64:33 * 64].reshape(17, 64)
+        self.last_phase = out[self.num_items + 2048:self.num_items + 4096]
         ctas = out[self.num_items:n]
         return out[:self.num_items], ctas[ctas[:, 1] == -1]
 

@@ -66,6 +66,7 @@ def main():
     ap.add_argument("--groups", type=int, default=0)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--json")
+    ap.add_argument("--tile2", type=int, default=1)
     args = ap.parse_args()
     dev = torch.device("cuda", 0)
     spec = W.config(args.config)
@@ -89,7 +90,15 @@ def main():
     rep["ctas_per_sm"] = float(len(ctas) / max(1, len(np.unique(ctas[:, 0] >> 32))))
     rep["num_ctas"] = int(len(ctas))
     ev = getattr(op, "last_tile_events", None)
-    if ev is not None and ev[5, 2] != 0:
+    if ev is not None and op.plan_tables()["num_tile_items"] > 0 and ev[0, 0] != 0 and args.tile2:
+        # v2 tile events (CTA 0, slot 0): clock64 per block
+        names = ["s_ready", "ld_done", "max_done", "exp_done", "p_arrive", "s_issue", "pv_issue",
+                 "k_issue", "v_issue"]
+        t0 = ev[7, 0]
+        nb = int((ev[0] != 0).sum())
+        rep["tile2_events_cycles"] = {nm: [int(x - t0) if x else 0 for x in ev[i, :min(nb, 24)]]
+                                      for i, nm in enumerate(names)}
+    elif ev is not None and ev[5, 2] != 0:
         t0 = ev[5, 2]
         names = ["prod_issue", "s_issue", "soft_s_ready", "p_arrive", "pv_issue", "misc",
                  "k_wait_start", "v_wait_start", "v_issue"]
@@ -104,6 +113,12 @@ def main():
         names = ["k_issue", "v_issue", "s_issue", "pv_issue", "soft_s_ready", "p_arrive", "item_end", "epi_ofull_wait", "epi_ofull_done", "epi_finish_done", "ld_done", "max_done", "bar1_done", "exp_done", "odone_done", "pstore_done", "fence_done"]
         rep["dec0_events_cycles"] = {nm: [int(x - t0) if x else 0 for x in dv[i, :min(nb, 16)]]
                                      for i, nm in enumerate(names)}
+    ph = getattr(op, "last_phase", None)
+    if ph is not None and (ph[:, 3] != 0).any():
+        st = tr[:, 2].min()
+        sel = ph[:, 3] != 0
+        rep["tile_phase_end_us_pct"] = {nm: [float(x) for x in np.percentile((ph[sel, i] - st) / 1e3, [0, 50, 90, 100])]
+                                        for i, nm in enumerate(["softmax", "support", "merge", "barrier"])}
     rep["config"] = args.config
     print(json.dumps(rep, indent=1))
     if args.json:
