@@ -49,6 +49,7 @@ struct alignas(16) Shared {
   uint64_t s_full, s_free, p_full[2], o_done, o_full[2], o_empty[2];
   int item_idx[2];
   float red[2][4][kR];  // per-warp partial row maxima (double-buffered by block parity) / sums
+  int item_fast[2];     // producer's fast-merge decision per item slot (see NoFast)
   // merge queue: softmax thread 0 appends the units this CTA completes, warps 6-7 merge them
   dev::MergeQueue mq;
 };
@@ -78,8 +79,23 @@ __device__ __forceinline__ void enqueue_merge(Shared* sh, int idx) { dev::mq_pus
 
 // Warps 6-7: arrive at / merge the queued items' units until the queue is closed and drained.
 template <typename MergeUnit>
-__device__ __forceinline__ void merge_loop(Shared* sh, MergeUnit&& merge_unit) {
-  dev::mq_drain(&sh->mq, 1, merge_unit);
+__device__ __forceinline__ void merge_loop(const KParams& p, Shared* sh, MergeUnit&& merge_unit) {
+  int n = 0;
+  dev::mq_drain(&sh->mq, 1, [&](int task) {
+    // diagnostics: CTA 0, pipeline 0: start / end clock of the first 32 tasks per merge warp
+    const bool rec = false;
+    const int slot = ((threadIdx.x >> 5) & 1) * 32 + n;
+    long long t0 = 0;
+    if (rec) asm volatile("mov.u64 %0, %%clock64;" : "=l"(t0));
+    merge_unit(task);
+    if (rec) {
+      long long t1;
+      asm volatile("mov.u64 %0, %%clock64;" : "=l"(t1));
+      p.trace[(int64_t(p.num_items) + 4096) * 4 + 34 * 64 + slot] = t0;
+      p.trace[(int64_t(p.num_items) + 4096) * 4 + 35 * 64 + slot] = t1;
+    }
+    ++n;
+  });
 }
 
 // Diagnostics: clock64 of per-block events of CTA 0's first 64 decode blocks, after
@@ -140,9 +156,24 @@ __device__ __forceinline__ int block_nvalid(const ItemT& it, int nbA, int j) {
 // The decode pipeline. `load(idx)` returns the ItemRec of queue entry idx;
 // `finish` / `merge_unit` are provided by the kernel (output + merges). Pipeline
 // `pi` runs on warps 8*pi .. 8*pi+7 (the v2 kernel runs two per CTA).
-template <typename T, typename LoadItem, typename Finish, typename MergeUnit>
+// `fast` (see psa_kernel.cu, DecFast): an item whose only merge unit has one other
+// contributor that already arrived (typically the group's prefix tile) merges that
+// contributor's partial in registers and writes the final rows itself — no partial
+// rows, no arrival task, no merge. fast.probe(it) (thread 0) / fast.fetch(it, t, R,
+// Other&) (all threads, after block 0's barrier) / fast.finish(it, t, R, m, L, ov, o).
+struct NoFast {
+  struct Other {};
+  template <typename I> __device__ int probe(const I&) const { return 0; }
+  template <typename I> __device__ void fetch(const I&, int, int, Other&) const {}
+  template <typename I>
+  __device__ void finish(const I&, int, int, const float (&)[kR], const float (&)[kR],
+                         const float (&)[kR], const Other&) const {}
+};
+
+template <typename T, typename LoadItem, typename Finish, typename MergeUnit, typename Fast = NoFast>
 __device__ void run(const KParams& p, uint8_t* smem_raw, Shared* sh, uint32_t tmem, int pi,
-                    LoadItem&& load_item_at, Finish&& finish, MergeUnit&& merge_unit) {
+                    LoadItem&& load_item_at, Finish&& finish, MergeUnit&& merge_unit,
+                    const Fast& fast = Fast()) {
   const int warp = (threadIdx.x >> 5) - 8 * pi, lane = threadIdx.x & 31;
   const Geo G = carve(smem_raw, p.dec_slots);
   const uint32_t NSL = uint32_t(p.dec_slots);
@@ -150,13 +181,28 @@ __device__ void run(const KParams& p, uint8_t* smem_raw, Shared* sh, uint32_t tm
 
   if (warp == 4) {
     // ================= producer =================
+    // Software-pipelined over items: the queue slot of item k+2 (global atomic) and
+    // the record of item k+1 are in flight while item k's K/V loads are issued (and
+    // wait for ring slots). Q rows come by TMA (whole tokens, SW128) on the item_full
+    // barrier, so a 2-block decode item pays no dependent global round trips before
+    // its first K/V load.
+    const T* Q = static_cast<const T*>(p.q);
+    int raw = 0;
+    if (lane == 0) raw = p.n_tile_items + atomicAdd(&p.ctrl->next_vec, 1);
+    int idx = __shfl_sync(0xffffffffu, raw, 0);
+    if (lane == 0) raw = p.n_tile_items + atomicAdd(&p.ctrl->next_vec, 1);  // item k + 1
+    decltype(load_item_at(0)) it{};
+    int64_t tok0 = 0;
+    if (idx < n_items) {
+      it = load_item_at(idx);
+      tok0 = __ldg(p.group_tok0 + it.g);
+    }
     uint32_t c = 0;  // K/V slot loads issued
     for (uint32_t k = 0;; ++k) {
       const uint32_t q = k & 1;
+      int fast_k = 0;
+      if (lane == 0 && idx < n_items) fast_k = fast.probe(it);  // latency overlaps the wait
       dev::mbar_wait(&sh->item_empty[q], ((k >> 1) & 1) ^ 1);
-      int idx = 0;
-      if (lane == 0) idx = p.n_tile_items + atomicAdd(&p.ctrl->next_vec, 1);
-      idx = __shfl_sync(0xffffffffu, idx, 0);
       if (idx >= n_items) {
         if (lane == 0) {
           sh->item_idx[q] = -1;
@@ -164,12 +210,9 @@ __device__ void run(const KParams& p, uint8_t* smem_raw, Shared* sh, uint32_t tm
         }
         break;
       }
-      const auto it = load_item_at(idx);
-      // Q rows of the item -> K-major SW128 [16 rows][128] (2 chunks of 64), lane-parallel
-      {
-        const int64_t tok0 = __ldg(p.group_tok0 + it.g);
-        const T* Q = static_cast<const T*>(p.q);
-        uint8_t* qs = G.q(q);
+      uint8_t* qs = G.q(q);
+      const bool q_tma = p.dec_q_tma && (it.row0 % p.gqa) == 0;
+      if (!q_tma) {  // Q rows -> K-major SW128 [16 rows][128] (2 chunks of 64), lane-parallel
         for (int u = lane; u < kN * 16; u += 32) {  // 16-byte units: row u/16, unit u%16
           const int r = u >> 4, cu = u & 15;
           uint4 v = make_uint4(0u, 0u, 0u, 0u);
@@ -183,9 +226,26 @@ __device__ void run(const KParams& p, uint8_t* smem_raw, Shared* sh, uint32_t tm
         dev::fence_proxy_async_smem();
         __syncwarp();
       }
+      // next item: its index (claimed one iteration ago) and its record
+      const int next = __shfl_sync(0xffffffffu, raw, 0);
+      if (lane == 0 && next < n_items) raw = p.n_tile_items + atomicAdd(&p.ctrl->next_vec, 1);
+      decltype(load_item_at(0)) it_next{};
+      int64_t tok_next = 0;
+      if (next < n_items) {
+        it_next = load_item_at(next);
+        tok_next = __ldg(p.group_tok0 + it_next.g);
+      }
       if (lane == 0) {
         sh->item_idx[q] = idx;
-        dev::mbar_arrive(&sh->item_full[q]);
+        sh->item_fast[q] = fast_k;
+        if (q_tma) {
+          const int t0 = int(tok0 + it.row0 / p.gqa);
+          dev::mbar_arrive_expect_tx(&sh->item_full[q], uint32_t(kQBytes));
+          dev::tma_load_4d(qs, &p.tmd_q, &sh->item_full[q], 0, 0, it.h, t0);
+          dev::tma_load_4d(qs + kN * 128, &p.tmd_q, &sh->item_full[q], 64, 0, it.h, t0);
+        } else {
+          dev::mbar_arrive(&sh->item_full[q]);
+        }
         int nbA, nb;
         int64_t pbase, dbase;
         item_blocks(p, it, nbA, nb, pbase, dbase);
@@ -206,6 +266,9 @@ __device__ void run(const KParams& p, uint8_t* smem_raw, Shared* sh, uint32_t tm
         }
       }
       __syncwarp();
+      idx = next;
+      it = it_next;
+      tok0 = tok_next;
     }
   } else if (warp == 5) {
     // ================= MMA issuer =================
@@ -306,7 +369,7 @@ __device__ void run(const KParams& p, uint8_t* smem_raw, Shared* sh, uint32_t tm
       }
     }
   } else if (warp >= 6) {
-    merge_loop(sh, merge_unit);
+    merge_loop(p, sh, merge_unit);
   } else if (warp < 4) {
     // ================= softmax + epilogue =================
     const int t = threadIdx.x - 256 * pi;
@@ -330,6 +393,11 @@ __device__ void run(const KParams& p, uint8_t* smem_raw, Shared* sh, uint32_t tm
       int64_t pbase, dbase;
       item_blocks(p, it, nbA, nb, pbase, dbase);
       const int R = it.nrows;
+      // fast merge decided by the producer (its acquire load + this item_full wait order
+      // the other contributor's partial rows before the fetch); fetched now, used at the end
+      const bool fast_on = sh->item_fast[q] != 0;
+      typename Fast::Other other;
+      if (fast_on) fast.fetch(it, t, R, other);
       // rows >= R keep m = 0 and x = -inf: their exps are exactly 0, no NaN, and
       // every row's arithmetic stays branch-free (the rows interleave for ILP).
       float m[kR], lp[kR];
@@ -365,6 +433,7 @@ __device__ void run(const KParams& p, uint8_t* smem_raw, Shared* sh, uint32_t tm
         }
         if (t == 0) dbg(p, 11, g);
         named_sync_softmax(pi);  // red[g & 1] is rewritten two blocks later, after another barrier
+
         if (t == 0) dbg(p, 12, g);
         const float (&rd)[4][kR] = sh->red[g & 1];
         float alpha[kR];
@@ -453,7 +522,8 @@ __device__ void run(const KParams& p, uint8_t* smem_raw, Shared* sh, uint32_t tm
       float ov[kR];
 #pragma unroll
       for (int r = 0; r < kR; ++r) ov[r] = __uint_as_float(o[r]);
-      finish(it, idx, t, R, m, L, ov);  // output, or partial rows queued for arrival
+      if (fast_on) fast.finish(it, t, R, m, L, ov, other);  // merged in registers: final rows
+      else finish(it, idx, t, R, m, L, ov);  // output, or partial rows queued for arrival
       if (t == 0) dbg(p, 9, g - 1);
       named_sync_softmax(pi);      // red[] reuse + item slot release after everyone finished
       if (t == 0) dev::mbar_arrive(&sh->item_empty[q]);

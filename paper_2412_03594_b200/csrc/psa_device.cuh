@@ -222,6 +222,11 @@ __host__ __device__ constexpr uint32_t umma_idesc_f16(uint32_t ab_format, uint32
 }
 
 
+// gpu-scope acquire/release fence (lighter than the sequentially consistent
+// fence.sc.gpu behind __threadfence()); paired with relaxed atomics it forms the
+// release / acquire patterns of the PTX memory model.
+__device__ __forceinline__ void fence_acq_rel_gpu() { asm volatile("fence.acq_rel.gpu;" ::: "memory"); }
+
 // ---- CTA-local merge queue ------------------------------------------------------
 // Bounded MPMC ring in shared memory: threads that complete work push tasks, merge
 // warps pop them (and may push follow-up tasks). Every slot carries a sequence
@@ -303,7 +308,7 @@ __device__ __forceinline__ void mq_drain(MergeQueue* q, int closers, Task&& task
     ok = __shfl_sync(0xffffffffu, ok, 0);
     if (!ok) break;
     u = __shfl_sync(0xffffffffu, u, 0);
-    __threadfence();  // acquire: the task's partial rows were published before it was queued
+    fence_acq_rel_gpu();  // acquire: the task's partial rows were published before it was queued
     task(u);
     __syncwarp();
     if (lane == 0) {

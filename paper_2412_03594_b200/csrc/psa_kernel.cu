@@ -155,9 +155,9 @@ template <> __device__ __forceinline__ void store4<__half>(__half* dst, float4 v
 
 // Four consecutive columns (c % 4 == 0, dv % 4 == 0) of a final row, fp32 accumulate.
 template <typename T>
-__device__ __forceinline__ void write_final4(const KParams& p, int g, int h, int row, int c,
-                                             float M, float L, float4 O) {
-  const int64_t tok = __ldg(p.group_tok0 + g) + row / p.gqa;
+__device__ __forceinline__ void write_final4_t(const KParams& p, int64_t tok0, int h, int row,
+                                               int c, float M, float L, float4 O) {
+  const int64_t tok = tok0 + row / p.gqa;
   const int64_t idx = tok * p.Hq + (int64_t)h * p.gqa + row % p.gqa;
   if (p.flags & PSA_FLAG_PARTIAL_OUT) {
     store4<float>(static_cast<float*>(p.out) + idx * p.dv + c, O, 1.f);
@@ -172,6 +172,12 @@ __device__ __forceinline__ void write_final4(const KParams& p, int g, int h, int
     if (!(L > 0.f)) atomicOr(&p.ctrl->error, 1);
     if (p.lse) p.lse[idx] = (M + log2f(L)) * Dom<float>::kToNat;
   }
+}
+
+template <typename T>
+__device__ __forceinline__ void write_final4(const KParams& p, int g, int h, int row, int c,
+                                             float M, float L, float4 O) {
+  write_final4_t<T>(p, __ldg(p.group_tok0 + g), h, row, c, M, L, O);
 }
 
 // Emits one combined (row, column) value of an item: to the workspace when the
@@ -481,6 +487,7 @@ __device__ __forceinline__ void merge_chunk_warp(const KParams& p, int u, int r0
   const int32_t* U = p.units + (int64_t)u * kUnitWords;
   const int g = __ldg(U + kUnGroup), h = __ldg(U + kUnHead), row0 = __ldg(U + kUnRow0);
   const int cb = __ldg(U + kUnContribBegin), cc = __ldg(U + kUnContribCount);
+  const int64_t tok0 = __ldg(p.group_tok0 + g);
   const float* WO = static_cast<const float*>(p.ws_o);
   const float2* WML = static_cast<const float2*>(p.ws_ml);
   const int dv = p.dv, c = lane * 4;
@@ -489,15 +496,26 @@ __device__ __forceinline__ void merge_chunk_warp(const KParams& p, int u, int r0
   if (lane < nr * cc) {
     const int r = lane / cc, i = lane - r * cc;
     wr = (int64_t)__ldg(p.contribs + cb + i) + r0 + r;
-    ml = __ldcg(WML + wr);
   }
+  // the partial rows' o are loaded together with their (m, l): one round trip
+  float4 v8[8];
+  if (cc <= 8) {
+    const int np0 = min(8 / cc, nr) * cc;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const int64_t wj = __shfl_sync(0xffffffffu, wr, j);
+      v8[j] = (j < np0 && c < dv) ? __ldcg(reinterpret_cast<const float4*>(WO + wj * dv + c))
+                                  : make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+  }
+  if (lane < nr * cc) ml = __ldcg(WML + wr);
   const float mv = ml.y > 0.f ? ml.x : -INFINITY;
   // per-row max over the row's cc lanes (lanes of a row are contiguous)
   float M = -INFINITY;
   const int my_r = lane / max(cc, 1);
   for (int i = 0; i < cc; ++i) M = fmaxf(M, __shfl_sync(0xffffffffu, mv, min(my_r * cc + i, 31)));
   const float f = ml.y > 0.f ? dev::ex2(ml.x - M) : 0.f;
-  const float fl = f * ml.y;
+  const float fl = __fmul_rn(f, ml.y);
   if (cc <= 8) {
     // groups of rg rows: rg * cc <= 8 (row, contribution) pairs, all loads in flight
     const int rg = 8 / cc;
@@ -509,23 +527,28 @@ __device__ __forceinline__ void merge_chunk_warp(const KParams& p, int u, int r0
       for (int j = 0; j < 8; ++j) {
         const int src = min(rb * cc + j, 31);
         fi[j] = j < np ? __shfl_sync(0xffffffffu, f, src) : 0.f;
-        const int64_t wj = __shfl_sync(0xffffffffu, wr, src);
-        v[j] = (j < np && fi[j] != 0.f && c < dv)
-                   ? __ldcg(reinterpret_cast<const float4*>(WO + wj * dv + c))
-                   : make_float4(0.f, 0.f, 0.f, 0.f);
+        if (rb == 0) {
+          v[j] = fi[j] != 0.f ? v8[j] : make_float4(0.f, 0.f, 0.f, 0.f);
+        } else {
+          const int64_t wj = __shfl_sync(0xffffffffu, wr, src);
+          v[j] = (j < np && fi[j] != 0.f && c < dv)
+                     ? __ldcg(reinterpret_cast<const float4*>(WO + wj * dv + c))
+                     : make_float4(0.f, 0.f, 0.f, 0.f);
+        }
       }
       for (int rr = 0; rr < rg && rb + rr < nr; ++rr) {
         float4 O = make_float4(0.f, 0.f, 0.f, 0.f);
         float L = 0.f;
 #pragma unroll
-        for (int j = 0; j < 8; ++j) {
+        for (int j = 0; j < 8; ++j) {  // contribution order; arithmetic pinned (DecFast)
           const bool mine = j >= rr * cc && j < (rr + 1) * cc;
           const float fj = mine ? fi[j] : 0.f;
-          O.x += fj * v[j].x; O.y += fj * v[j].y; O.z += fj * v[j].z; O.w += fj * v[j].w;
+          O.x = __fmaf_rn(fj, v[j].x, O.x); O.y = __fmaf_rn(fj, v[j].y, O.y);
+          O.z = __fmaf_rn(fj, v[j].z, O.z); O.w = __fmaf_rn(fj, v[j].w, O.w);
         }
-        for (int i = 0; i < cc; ++i) L += __shfl_sync(0xffffffffu, fl, min((rb + rr) * cc + i, 31));
+        for (int i = 0; i < cc; ++i) L = __fadd_rn(L, __shfl_sync(0xffffffffu, fl, min((rb + rr) * cc + i, 31)));
         const float Mr = __shfl_sync(0xffffffffu, M, min((rb + rr) * cc, 31));
-        if (c < dv) write_final4<T>(p, g, h, row0 + r0 + rb + rr, c, Mr, L, O);
+        if (c < dv) write_final4_t<T>(p, tok0, h, row0 + r0 + rb + rr, c, Mr, L, O);
       }
     }
     return;
@@ -554,7 +577,7 @@ __device__ __forceinline__ void merge_chunk_warp(const KParams& p, int u, int r0
       }
     }
     const float Mr = __shfl_sync(0xffffffffu, M, min(rr * cc, 31));
-    if (c < dv) write_final4<T>(p, g, h, row0 + r0 + rr, c, Mr, L, O);
+    if (c < dv) write_final4_t<T>(p, tok0, h, row0 + r0 + rr, c, Mr, L, O);
   }
 }
 
@@ -671,12 +694,21 @@ __device__ __forceinline__ void warp_arrive_and_merge(const KParams& p, const It
 // `on_last(u)` gets every unit this arrival completed (merge it now, or queue it so
 // several merge warps share a tile's units). Keeps the gpu-scope fence and the
 // merges off the softmax warps' critical path.
+__device__ __forceinline__ void dbg_clock(const KParams& p, int ev, int slot) {
+  if (slot >= 0 && (threadIdx.x & 31) == 0) {
+    long long t;
+    asm volatile("mov.u64 %0, %%clock64;" : "=l"(t));
+    p.trace[(int64_t(p.num_items) + 4096) * 4 + ev * 64 + slot] = t;
+  }
+}
+
 template <typename OnLast>
 __device__ __forceinline__ void warp_arrive_rows(const KParams& p, const ItemRec& it, int r0,
-                                                 int r1, OnLast&& on_last) {
+                                                 int r1, OnLast&& on_last, int dslot = -1) {
   const int lane = threadIdx.x & 31;
-  __threadfence();
+  dev::fence_acq_rel_gpu();
   __syncwarp();
+  dbg_clock(p, 36, dslot);
   for (int base = it.u0; base < it.u1; base += 32) {
     const int u = base + lane;
     bool is_last = false;
@@ -692,7 +724,9 @@ __device__ __forceinline__ void warp_arrive_rows(const KParams& p, const ItemRec
       }
     }
     uint32_t last = __ballot_sync(0xffffffffu, is_last);
-    if (last) __threadfence();  // acquire: the other contributors' partial rows
+    dbg_clock(p, 37, dslot);
+    if (last) dev::fence_acq_rel_gpu();  // acquire: the other contributors' partial rows
+    dbg_clock(p, 38, dslot);
     while (last) {
       const int bit = __ffs(last) - 1;
       last &= last - 1;
@@ -700,6 +734,84 @@ __device__ __forceinline__ void warp_arrive_rows(const KParams& p, const ItemRec
     }
   }
 }
+
+// Decode items whose single merge unit has exactly one other contributor (the
+// group's prefix tile chunk) that has already arrived: the item merges that partial
+// in registers (thread t = value column t) with the same arithmetic, in the same
+// contribution order, as merge_chunk_warp — so the result is bit-identical whichever
+// side finishes last — and writes the final rows; it never publishes a partial.
+template <typename T>
+struct DecFast {
+  const KParams& p;
+  struct Other {
+    float m[dec::kR], l[dec::kR], o[dec::kR];
+    int first;  // the other contribution precedes this item's in contribution order
+  };
+  __device__ int probe(const ItemRec& it) const {
+    if (it.ws_row < 0 || it.u1 - it.u0 != 1) return 0;
+    const int32_t* U = p.units + (int64_t)it.u0 * kUnitWords;
+    if (__ldg(U + kUnRows) != it.nrows || __ldg(U + kUnContribCount) != 2 ||
+        __ldg(U + kUnRow0) != it.row0)
+      return 0;
+    int cnt;
+    asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(cnt) : "l"(p.unit_cnt + it.u0) : "memory");
+    return cnt == 1 ? 1 : 0;
+  }
+  __device__ void fetch(const ItemRec& it, int t, int R, Other& o) const {
+    const int32_t* U = p.units + (int64_t)it.u0 * kUnitWords;
+    const int cb = __ldg(U + kUnContribBegin);
+    const int c0 = __ldg(p.contribs + cb), c1 = __ldg(p.contribs + cb + 1);
+    o.first = c0 != it.ws_row;
+    const int64_t base = o.first ? c0 : c1;
+    const float* WO = static_cast<const float*>(p.ws_o);
+    const float2* WML = static_cast<const float2*>(p.ws_ml);
+#pragma unroll
+    for (int r = 0; r < dec::kR; ++r) {
+      if (r < R) {
+        const float2 ml = __ldcg(WML + base + r);
+        o.m[r] = ml.x;
+        o.l[r] = ml.y;
+        o.o[r] = __ldcg(WO + (base + r) * 128 + t);
+      }
+    }
+  }
+  __device__ void finish(const ItemRec& it, int t, int R, const float (&m)[dec::kR],
+                         const float (&L)[dec::kR], const float (&ov)[dec::kR],
+                         const Other& o) const {
+    const int64_t tok0 = __ldg(p.group_tok0 + it.g);
+    const bool partial_out = p.flags & PSA_FLAG_PARTIAL_OUT;
+#pragma unroll
+    for (int r = 0; r < dec::kR; ++r) {
+      if (r >= R) continue;
+      // contributions in order: (m0, l0, o0) then (m1, l1, o1)
+      const float m0 = o.first ? o.m[r] : m[r], l0 = o.first ? o.l[r] : L[r];
+      const float o0 = o.first ? o.o[r] : ov[r];
+      const float m1 = o.first ? m[r] : o.m[r], l1 = o.first ? L[r] : o.l[r];
+      const float o1 = o.first ? ov[r] : o.o[r];
+      const float M = fmaxf(fmaxf(-INFINITY, l0 > 0.f ? m0 : -INFINITY), l1 > 0.f ? m1 : -INFINITY);
+      const float f0 = l0 > 0.f ? dev::ex2(m0 - M) : 0.f;
+      const float f1 = l1 > 0.f ? dev::ex2(m1 - M) : 0.f;
+      const float Ls = __fadd_rn(__fadd_rn(0.f, __fmul_rn(f0, l0)), __fmul_rn(f1, l1));
+      const float O = __fmaf_rn(f1, o1, __fmaf_rn(f0, o0, 0.f));
+      const int row = it.row0 + r;
+      const int64_t idx = (tok0 + row / p.gqa) * p.Hq + (int64_t)it.h * p.gqa + row % p.gqa;
+      if (partial_out) {
+        static_cast<float*>(p.out)[idx * 128 + t] = O;
+        if (t == 0) {
+          static_cast<float*>(p.m_out)[idx] = M * Dom<float>::kToNat;
+          static_cast<float*>(p.l_out)[idx] = Ls;
+        }
+        continue;
+      }
+      static_cast<T*>(p.out)[idx * 128 + t] = from_acc<T>(O * (1.f / Ls));
+      if (t == 0) {
+        if (!(Ls > 0.f)) atomicOr(&p.ctrl->error, 1);
+        if (p.lse) p.lse[idx] = (M + log2f(Ls)) * Dom<float>::kToNat;
+      }
+    }
+    if (t == 0) p.unit_cnt[it.u0] = 0;  // every contributor arrived: reset for the next launch
+  }
+};
 
 // End of a decode item (thread t = value column t of the item's <= 8 rows): the
 // partial rows + arrival at the merge units, or the final output.
@@ -931,9 +1043,11 @@ __global__ void __launch_bounds__(kV2Threads, 1) psa_v2(const __grid_constant__ 
   __shared__ tile2::Shared s_t2;
   __shared__ dec::Shared s_dec[2];
   __shared__ uint32_t s_tmem;
+  __shared__ int s_dbg_n;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t t_kernel0 = (p.trace_cap > 0 && threadIdx.x == 0) ? int64_t(globaltimer()) : 0;
   if (threadIdx.x == 0) {
+    s_dbg_n = 0;
     tile2::init(&s_t2);
     dec::init_barriers(&s_dec[0]);
     dec::init_barriers(&s_dec[1]);
@@ -958,7 +1072,17 @@ __global__ void __launch_bounds__(kV2Threads, 1) psa_v2(const __grid_constant__ 
   // that slot's rows) or ~u (merge unit u): a slot can complete dozens of units, so
   // they go back to the queue and all six merge warps share them.
   auto merge_now = [&](int u) { merge_unit_warp<T>(p, u); };
-  auto arrive_dec = [&](int idx) { warp_arrive_rows(p, load_at(idx), INT_MIN, INT_MAX, merge_now); };
+  auto arrive_dec = [&](int idx) {
+    int dslot = -1;  // diagnostics: CTA 0, pipeline 0, ticket < 64
+    if (p.trace_cap > 0 && blockIdx.x == 0 && threadIdx.x < 256) {
+      int n = 0;
+      if ((threadIdx.x & 31) == 0) n = atomicAdd(&s_dbg_n, 1);
+      n = __shfl_sync(0xffffffffu, n, 0);
+      if (n < 64) dslot = n;
+    }
+    warp_arrive_rows(p, load_at(idx), INT_MIN, INT_MAX, merge_now, dslot);
+    if (dslot >= 0) dbg_clock(p, 39, dslot);
+  };
   auto tile_task = [&](int task) {
     if (task < 0) {
       merge_unit_warp<T>(p, ~task);
@@ -981,10 +1105,10 @@ __global__ void __launch_bounds__(kV2Threads, 1) psa_v2(const __grid_constant__ 
 
   // diagnostics: per-CTA phase record {t(softmax done), t(producer/MMA done), t(merge
   // warps done), t(tile phase barrier passed)} at trace row num_items + 2048 + CTA
-  auto phase_mark = [&](int field) {
+  auto phase_mark = [&](int field, int row = 2048) {
     if (p.trace_cap > 0 && (threadIdx.x & 31) == 0)
       atomicMax(reinterpret_cast<unsigned long long*>(
-                    p.trace + (int64_t(p.num_items) + 2048 + blockIdx.x) * 4 + field),
+                    p.trace + (int64_t(p.num_items) + row + blockIdx.x) * 4 + field),
                 (unsigned long long)globaltimer());
   };
   if (p.use_tiles) {
@@ -1017,7 +1141,11 @@ __global__ void __launch_bounds__(kV2Threads, 1) psa_v2(const __grid_constant__ 
       dec_finish<T>(p, &s_dec[pi], it, idx, t, R, m, L, ov, pi);
     };
     dec::run<T>(p, smem + pi * half, &s_dec[pi], tmem + 64u * uint32_t(pi), pi, load_at, finish,
-                arrive_dec);
+                arrive_dec, DecFast<T>{p});
+    // diagnostics: decode-phase record at trace row num_items + 3072 + CTA:
+    // {softmax warps, producer, MMA warp, merge warps} done
+    const int rw = (warp & 7) < 4 ? 0 : (warp & 7) == 4 ? 1 : (warp & 7) == 5 ? 2 : 3;
+    phase_mark(rw, 3072);
   }
   __syncthreads();
   if (p.trace_cap > 0 && threadIdx.x == 0) trace_item(p, p.num_items + int(blockIdx.x), -1, t_kernel0);
@@ -1263,6 +1391,21 @@ int encode_tile_maps(KParams& p, int32_t dtype, int64_t T, int64_t prefix_keys,
     if (!e) e = encode_kv(&p.tm_vd, dt, p.vd, distinct_keys, p.Hkv, p.dv, 64, tile::kBN, true);
   }
   if (!e && (p.use_dec || p.use_v2)) {
+    std::memset(&p.tmd_q, 0, sizeof(p.tmd_q));
+    const int gqa = p.gqa;
+    p.dec_q_tma = 0;
+    if (gqa <= dec::kN && (dec::kN % gqa) == 0 && T > 0) {
+      cuuint64_t gdim[4] = {cuuint64_t(p.d), cuuint64_t(gqa), cuuint64_t(p.Hkv), cuuint64_t(T)};
+      cuuint64_t gstride[3] = {cuuint64_t(p.d) * 2, cuuint64_t(p.d) * gqa * 2,
+                               cuuint64_t(p.d) * p.Hq * 2};
+      cuuint32_t box[4] = {64, cuuint32_t(gqa), 1, cuuint32_t(dec::kN / gqa)};
+      cuuint32_t estr[4] = {1, 1, 1, 1};
+      CUresult r = encode_fn()(&p.tmd_q, dt, 4, const_cast<void*>(p.q), gdim, gstride, box, estr,
+                               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                               CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+      if (r != CUDA_SUCCESS) return int(cudaErrorInvalidValue);
+      p.dec_q_tma = 1;
+    }
     e = encode_kv(&p.tmd_kp, dt, p.kp, prefix_keys, p.Hkv, p.d, 64, dec::kBK, true);
     if (!e) e = encode_kv(&p.tmd_vp, dt, p.vp, prefix_keys, p.Hkv, p.dv, 64, dec::kBK, true);
     if (!e) e = encode_kv(&p.tmd_kd, dt, p.kd, distinct_keys, p.Hkv, p.d, 64, dec::kBK, true);

@@ -36,6 +36,9 @@ struct KParams {
   alignas(64) CUtensorMap tmd_vp;
   alignas(64) CUtensorMap tmd_kd;
   alignas(64) CUtensorMap tmd_vd;
+  // decode Q rows: q as 4-D (d, gqa, Hkv, T), (64, gqa, 1, 16 / gqa) boxes, 128-byte
+  // swizzle — one item's <= 16 stacked rows (whole tokens) per box pair
+  alignas(64) CUtensorMap tmd_q;
   const void* q;
   const void* kp;
   const void* vp;
@@ -68,6 +71,7 @@ struct KParams {
   int32_t dec_slots;     // decode K/V ring slots (ditto)
   int32_t use_v2;       // v2 kernel: 1 CTA/SM, paired tile slots + two decode pipelines
   int32_t dec_pipes;    // v2: decode pipelines per CTA (2; 1 under PSA_DEBUG bit 0)
+  int32_t dec_q_tma;    // tmd_q is valid (gqa is a power of two <= 16)
   double scale;
   int64_t* trace;        // diagnostics: per item {cta | smid << 32, kind, t_start, t_end}
 };

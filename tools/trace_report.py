@@ -119,6 +119,19 @@ def main():
         sel = ph[:, 3] != 0
         rep["tile_phase_end_us_pct"] = {nm: [float(x) for x in np.percentile((ph[sel, i] - st) / 1e3, [0, 50, 90, 100])]
                                         for i, nm in enumerate(["softmax", "support", "merge", "barrier"])}
+    dp = getattr(op, "last_dec_phase", None)
+    if dp is not None and (dp[:, 0] != 0).any():
+        st = tr[:, 2].min()
+        sel = dp[:, 0] != 0
+        rep["dec_phase_end_us_pct"] = {nm: [float(x) for x in np.percentile((dp[sel, i] - st) / 1e3, [0, 50, 90, 100])]
+                                       for i, nm in enumerate(["softmax", "producer", "mma", "merge"])}
+    mt = getattr(op, "last_merge_tasks", None)
+    if mt is not None and (mt[0] != 0).any():
+        sel = (mt[0] != 0) & (mt[3] != 0)
+        rep["dec_arrival_cycles_p50"] = {
+            "fence": 0, "atomic": float(np.median(mt[1, sel] - mt[0, sel])),
+            "fence2": float(np.median(mt[2, sel] - mt[1, sel])),
+            "merge": float(np.median(mt[3, sel] - mt[2, sel])), "n": int(sel.sum())}
     rep["config"] = args.config
     print(json.dumps(rep, indent=1))
     if args.json:
