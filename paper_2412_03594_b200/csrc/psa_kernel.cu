@@ -1271,6 +1271,7 @@ int launch_v2(const KParams& p_in, int32_t num_sms, void* stream) {
   const char* dbg_env = std::getenv("PSA_DEBUG");
   const int dbg = dbg_env ? std::atoi(dbg_env) : 0;
   p.dec_pipes = (dbg & 1) ? 1 : 2;
+  p.tile_pp = (dbg & 32) ? 0 : 1;
   if (dbg & 2) p.dec_slots = 2;
   size_t smem = 0;
   if (p.use_tiles) smem = tile2::smem_bytes(p.tile_stages);

@@ -72,6 +72,7 @@ struct KParams {
   int32_t use_v2;       // v2 kernel: 1 CTA/SM, paired tile slots + two decode pipelines
   int32_t dec_pipes;    // v2: decode pipelines per CTA (2; 1 under PSA_DEBUG bit 0)
   int32_t dec_q_tma;    // tmd_q is valid (gqa is a power of two <= 16)
+  int32_t tile_pp;      // v2 single-slot tile items ping-pong S buffers (0 under PSA_DEBUG bit 5)
   double scale;
   int64_t* trace;        // diagnostics: per item {cta | smid << 32, kind, t_start, t_end}
 };

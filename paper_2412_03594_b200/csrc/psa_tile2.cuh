@@ -54,6 +54,7 @@ struct Shared {
   uint64_t q_full, q_empty;
   uint64_t ring_full[kMaxRing], ring_empty[kMaxRing];
   uint64_t s_full[2], p_full[2], o_full[2], o_empty[2];
+  uint64_t pv_done;  // single-slot items: one phase per PV (the softmax's O-rescale wait)
   int item_idx[2];
   dev::MergeQueue mq;
 };
@@ -71,6 +72,7 @@ __device__ __forceinline__ void init(Shared* s) {
     dev::mbar_init(&s->o_full[i], 1);
     dev::mbar_init(&s->o_empty[i], 4);
   }
+  dev::mbar_init(&s->pv_done, 1);
   dev::mbar_init(&s->q_full, 1);
   dev::mbar_init(&s->q_empty, 1);
   for (int i = 0; i < kMaxRing; ++i) {
@@ -299,7 +301,7 @@ __device__ void run_support(const KParams& p, uint8_t* smem_raw, Shared* sh, uin
       const uint32_t idesc_s = dev::umma_idesc_f16(fmt, kM, kBN, 0, 0);
       const uint32_t idesc_o = dev::umma_idesc_f16(fmt, kM, kD, 0, 1);
       uint32_t gb = 0;       // K/V blocks consumed (ring position 2 * gb)
-      uint32_t nblk[2] = {0u, 0u};  // blocks processed per slot (p_full phases)
+      uint32_t nblk[2] = {0u, 0u};  // p_full[b] phases consumed (either mode)
       uint32_t nitem[2] = {0u, 0u}; // items processed per slot (o_empty phases)
       for (uint32_t k = 0;; ++k) {
         const uint32_t q = k & 1;
@@ -314,20 +316,21 @@ __device__ void run_support(const KParams& p, uint8_t* smem_raw, Shared* sh, uin
         const int ns = it.nrows > tile_rows ? 2 : 1;
         dev::mbar_wait(&sh->q_full, k & 1);
         dev::tc_fence_after();
-        auto issue_pv = [&](int i, uint32_t vslot, bool first) {
-          // O_i (+)= P_i V: 8 K-steps of 16 keys; A = P_i in TMEM (bf16 pairs)
+        // O_o (+)= P V: 8 K-steps of 16 keys; A = P in TMEM (bf16 pairs) in S buffer pb
+        auto issue_pv = [&](int pb, int o, uint32_t vslot, bool first) {
           const uint32_t v_addr = dev::smem_u32(G.slot(vslot));
-          const uint32_t tP = tmem + uint32_t(i) * 128, tO = tmem + kTmemO + uint32_t(i) * 128;
+          const uint32_t tP = tmem + uint32_t(pb) * 128, tO = tmem + kTmemO + uint32_t(o) * 128;
 #pragma unroll
           for (int kk = 0; kk < kBN / 16; ++kk) {
             const uint64_t b = dev::umma_desc_sw128(v_addr + kk * (16 * 128), kBN * 128, 1024);
             dev::mma_f16_ts(tO, tP + kk * 8, b, idesc_o, (!first || kk > 0) ? 1u : 0u);
           }
         };
-        auto issue_s = [&](int i, uint32_t kslot) {
+        // S buffer sb = Q_qi K^T
+        auto issue_s = [&](int qi, int sb, uint32_t kslot) {
           const uint32_t k_addr = dev::smem_u32(G.slot(kslot));
-          const uint32_t q_addr = dev::smem_u32(G.q(i));
-          const uint32_t tS = tmem + uint32_t(i) * 128;
+          const uint32_t q_addr = dev::smem_u32(G.q(qi));
+          const uint32_t tS = tmem + uint32_t(sb) * 128;
 #pragma unroll
           for (int kk = 0; kk < kD / 16; ++kk) {
             const uint32_t ch = kk >> 2, w = (kk & 3) * 32;
@@ -335,33 +338,35 @@ __device__ void run_support(const KParams& p, uint8_t* smem_raw, Shared* sh, uin
             const uint64_t b = dev::umma_desc_sw128(k_addr + ch * (kBN * 128) + w, 16, 1024);
             dev::mma_f16_ss(tS, a, b, idesc_s, kk > 0 ? 1u : 0u);
           }
-          dev::mma_commit(&sh->s_full[i]);
+          dev::mma_commit(&sh->s_full[sb]);
         };
-        for (int n = 0; n < nb; ++n) {
-          const uint32_t cK = 2 * (gb + n), sK = cK % NR;
-          const uint32_t cV = cK - 1, sV = cV % NR;  // V_{n-1}
-          dev::mbar_wait(&sh->ring_full[sK], (cK / NR) & 1);
-          if (n > 0) dev::mbar_wait(&sh->ring_full[sV], (cV / NR) & 1);
-          dev::tc_fence_after();
-          for (int i = 0; i < ns; ++i) {
-            if (n > 0) {
-              if (n == 1) {  // first PV of this item overwrites O_i: the WG read the last one
-                dev::mbar_wait(&sh->o_empty[i], (nitem[i] & 1) ^ 1);
+        if (ns == 2 || p.tile_pp == 0) {
+          // two slots share every K/V block: per block n, slot i: PV_i(n-1) then S_i(n)
+          // (S_i(n) overwrites P_i(n-1); MMAs of one thread execute in issue order)
+          for (int n = 0; n < nb; ++n) {
+            const uint32_t cK = 2 * (gb + n), sK = cK % NR;
+            const uint32_t cV = cK - 1, sV = cV % NR;  // V_{n-1}
+            dev::mbar_wait(&sh->ring_full[sK], (cK / NR) & 1);
+            if (n > 0) dev::mbar_wait(&sh->ring_full[sV], (cV / NR) & 1);
+            dev::tc_fence_after();
+            for (int i = 0; i < ns; ++i) {
+              if (n > 0) {
+                if (n == 1) {  // first PV of this item overwrites O_i: the WG read the last one
+                  dev::mbar_wait(&sh->o_empty[i], (nitem[i] & 1) ^ 1);
+                }
+                dev::mbar_wait(&sh->p_full[i], nblk[i] & 1);
+                ++nblk[i];
+                dev::tc_fence_after();
+                if (i == 0) dbg(p, 6, gb + n - 1);
+                issue_pv(i, i, sV, n == 1);
               }
-              dev::mbar_wait(&sh->p_full[i], nblk[i] & 1);
-              ++nblk[i];
-              dev::tc_fence_after();
-              if (i == 0) dbg(p, 6, gb + n - 1);
-              issue_pv(i, sV, n == 1);
+              if (i == 0) dbg(p, 5, gb + n);
+              issue_s(i, i, sK);
             }
-            if (i == 0) dbg(p, 5, gb + n);
-            issue_s(i, sK);
+            if (n > 0) dev::mma_commit(&sh->ring_empty[sV]);
+            dev::mma_commit(&sh->ring_empty[sK]);
           }
-          if (n > 0) dev::mma_commit(&sh->ring_empty[sV]);
-          dev::mma_commit(&sh->ring_empty[sK]);
-        }
-        dev::mma_commit(&sh->q_empty);  // every S of this item issued
-        {
+          dev::mma_commit(&sh->q_empty);  // every S of this item issued
           const uint32_t cV = 2 * (gb + nb) - 1, sV = cV % NR;
           dev::mbar_wait(&sh->ring_full[sV], (cV / NR) & 1);
           for (int i = 0; i < ns; ++i) {
@@ -369,10 +374,48 @@ __device__ void run_support(const KParams& p, uint8_t* smem_raw, Shared* sh, uin
             dev::mbar_wait(&sh->p_full[i], nblk[i] & 1);
             ++nblk[i];
             dev::tc_fence_after();
-            issue_pv(i, sV, nb == 1);
+            issue_pv(i, i, sV, nb == 1);
             dev::mma_commit(&sh->o_full[i]);
             ++nitem[i];
           }
+          dev::mma_commit(&sh->ring_empty[sV]);
+        } else {
+          // one slot: S ping-pongs between both S buffers (block n -> buffer n & 1), so
+          // S(n + 1) is computed while the softmax works on block n. Order: S(0), S(1),
+          // PV(0), S(2), PV(1), ...: S(n) overwrites P(n - 2) after PV(n - 2) was issued.
+          for (int n = 0; n < nb; ++n) {
+            const uint32_t cK = 2 * (gb + n), sK = cK % NR;
+            dev::mbar_wait(&sh->ring_full[sK], (cK / NR) & 1);
+            dev::tc_fence_after();
+            dbg(p, 5, gb + n);
+            issue_s(0, n & 1, sK);
+            dev::mma_commit(&sh->ring_empty[sK]);
+            if (n == nb - 1) dev::mma_commit(&sh->q_empty);  // every S of this item issued
+            if (n > 0) {
+              const uint32_t cV = cK - 1, sV = cV % NR;  // V_{n-1}
+              dev::mbar_wait(&sh->ring_full[sV], (cV / NR) & 1);
+              if (n == 1) dev::mbar_wait(&sh->o_empty[0], (nitem[0] & 1) ^ 1);
+              const int b = (n - 1) & 1;
+              dev::mbar_wait(&sh->p_full[b], nblk[b] & 1);
+              ++nblk[b];
+              dev::tc_fence_after();
+              dbg(p, 6, gb + n - 1);
+              issue_pv(b, 0, sV, n == 1);
+              dev::mma_commit(&sh->pv_done);
+              dev::mma_commit(&sh->ring_empty[sV]);
+            }
+          }
+          const uint32_t cV = 2 * (gb + nb) - 1, sV = cV % NR;  // V_{nb-1}
+          dev::mbar_wait(&sh->ring_full[sV], (cV / NR) & 1);
+          if (nb == 1) dev::mbar_wait(&sh->o_empty[0], (nitem[0] & 1) ^ 1);
+          const int b = (nb - 1) & 1;
+          dev::mbar_wait(&sh->p_full[b], nblk[b] & 1);
+          ++nblk[b];
+          dev::tc_fence_after();
+          issue_pv(b, 0, sV, nb == 1);
+          dev::mma_commit(&sh->pv_done);
+          dev::mma_commit(&sh->o_full[0]);
+          ++nitem[0];
           dev::mma_commit(&sh->ring_empty[sV]);
         }
         gb += nb;
@@ -391,10 +434,12 @@ __device__ void run_softmax(const KParams& p, Shared* sh, uint32_t tmem, LoadIte
     const int i = warp >> 2;
     const int row = threadIdx.x & 127;
     const uint32_t lane_base = uint32_t((warp & 3) * 32) << 16;
-    const uint32_t tS = tmem + uint32_t(i) * 128 + lane_base;
     const uint32_t tO = tmem + kTmemO + uint32_t(i) * 128 + lane_base;
     const float sc = float(p.scale) * 1.4426950408889634f;
     uint32_t nblk = 0, nitem = 0;
+    // s_full[b] phases consumed as seen by this WG (the other WG / mode consumes some
+    // of buffer 1's), and pv_done phases of single-slot items before the current one
+    uint32_t hs[2] = {0u, 0u}, npv = 0;
     for (uint32_t k = 0;; ++k) {
       const uint32_t q = k & 1;
       dev::mbar_wait(&sh->item_full[q], (k >> 1) & 1);
@@ -406,15 +451,23 @@ __device__ void run_softmax(const KParams& p, Shared* sh, uint32_t tmem, LoadIte
       named_sync(2 + i, 128);  // every thread of the WG has read item_idx[q]
       if (threadIdx.x % 128 == 0) dev::mbar_arrive(&sh->item_empty[q]);
       const int slot_rows = i == 0 ? min(it.nrows, tile_rows) : it.nrows - tile_rows;
-      if (slot_rows <= 0) continue;
       int nbA, nb;
       int64_t pbase, dbase;
       item_shape(p, it, nbA, nb, pbase, dbase);
+      const bool two = it.nrows > tile_rows;
+      const bool pp = !two && p.tile_pp != 0;  // single slot: S ping-pong over both buffers
+      if (slot_rows <= 0) {  // WG1, single-slot item: WG0 uses S buffer 1 for odd blocks
+        if (pp) hs[1] += uint32_t(nb) >> 1;
+        continue;
+      }
       float m = -INFINITY, l0 = 0.f, l1 = 0.f;
       for (int n = 0; n < nb; ++n, ++nblk) {
         const int nvalid = n < nbA ? min(kBN, it.pk1 - it.pk0 - n * kBN)
                                    : min(kBN, it.dk1 - it.dk0 - (n - nbA) * kBN);
-        dev::mbar_wait(&sh->s_full[i], nblk & 1);
+        const int b = pp ? (n & 1) : i;  // S buffer of this block
+        dev::mbar_wait(&sh->s_full[b], hs[b] & 1);
+        ++hs[b];
+        const uint32_t tS = tmem + uint32_t(b) * 128 + lane_base;
         const bool ev = threadIdx.x == 0;
         if (ev) dbg(p, 0, nblk);
         dev::tc_fence_after();
@@ -487,8 +540,13 @@ __device__ void run_softmax(const KParams& p, Shared* sh, uint32_t tmem, LoadIte
           dev::tmem_st32(tS + 32, hi);
         }
         if (__any_sync(0xffffffffu, rescale)) {
-          // O_i holds PV_0..PV_{n-1} (complete: S_n was issued after PV_{n-1}, and
-          // PV_n waits for this WG's p_full)
+          // O_i must hold PV(0 .. n-1) complete. Two slots: S_i(n) was issued after
+          // PV_i(n-1). One slot: S(n) only follows PV(n-2), so wait for PV(n-1) (PV(n)
+          // waits for this WG's p_full, so the parity cannot alias).
+          if (pp && n > 0) {
+            dev::mbar_wait(&sh->pv_done, (npv + uint32_t(n) - 1) & 1);
+            dev::tc_fence_after();
+          }
 #pragma unroll 1
           for (int c = 0; c < kD; c += 32) {
             uint32_t o[32];
@@ -502,8 +560,13 @@ __device__ void run_softmax(const KParams& p, Shared* sh, uint32_t tmem, LoadIte
         dev::tmem_wait_st();
         dev::tc_fence_before();
         __syncwarp();
-        if (lane == 0) dev::mbar_arrive(&sh->p_full[i]);
+        if (lane == 0) dev::mbar_arrive(&sh->p_full[b]);
         if (ev) dbg(p, 4, nblk);
+      }
+      if (two) {
+        if (i == 0) hs[1] += uint32_t(nb);  // WG1 consumed buffer 1's phases
+      } else if (pp) {
+        npv += uint32_t(nb);
       }
       // ---------------- epilogue: O_i -> output / partial ----------------
       dev::mbar_wait(&sh->o_full[i], nitem & 1);
