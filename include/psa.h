@@ -45,7 +45,7 @@
 extern "C" {
 #endif
 
-#define PSA_ABI_VERSION 2
+#define PSA_ABI_VERSION 3
 
 typedef enum psa_status {
   PSA_OK = 0,
@@ -90,6 +90,22 @@ typedef struct psa_problem {
   float* lse;  /* optional [T,Hq] natural-log LSE = m + log(l) (NULL = skip) */
   void* m_out; /* PARTIAL_OUT only: [T,Hq] running max logit (accumulate type) */
   void* l_out; /* PARTIAL_OUT only: [T,Hq] shifted exp-sum (accumulate type) */
+  /* Paged KV cache (vLLM-style blocks; the reference's KVAllocator, scheduler.py:140-187,
+   * block_size 16 at scheduler.py:45). page_size == 0: the packed layout above.
+   * page_size in {16, 32, 64} (bf16/f16, d == dv == 128 only; else PSA_UNSUPPORTED):
+   * k_prefix/v_prefix and k_distinct/v_distinct are page caches
+   * [*_cache_rows, Hkv, d|dv] (the same cache may back both), and logical key j of
+   * group g's prefix lives at cache row
+   *   prefix_pages[pp(g) + j / page_size] * page_size + j % page_size,
+   *   pp(g) = sum_{g' < g} ceil(P_g' / page_size),
+   * likewise distinct key j of request r via distinct_pages and
+   * dp(r) = sum_{r' < r} ceil(D_r' / page_size). Page tables are device int32. */
+  int32_t page_size;
+  int32_t reserved0;
+  const int32_t* prefix_pages;
+  const int32_t* distinct_pages;
+  int64_t prefix_cache_rows;
+  int64_t distinct_cache_rows;
 } psa_problem;
 
 typedef struct psa_plan_opts {

@@ -32,6 +32,9 @@ class Problem(C.Structure):
         ("q", C.c_void_p), ("k_prefix", C.c_void_p), ("v_prefix", C.c_void_p),
         ("k_distinct", C.c_void_p), ("v_distinct", C.c_void_p),
         ("out", C.c_void_p), ("lse", C.c_void_p), ("m_out", C.c_void_p), ("l_out", C.c_void_p),
+        ("page_size", C.c_int32), ("reserved0", C.c_int32),
+        ("prefix_pages", C.c_void_p), ("distinct_pages", C.c_void_p),
+        ("prefix_cache_rows", C.c_int64), ("distinct_cache_rows", C.c_int64),
     ]
 
 

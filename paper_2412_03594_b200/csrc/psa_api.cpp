@@ -23,6 +23,8 @@ struct psa_plan {
   bool use_dec = false;
   bool use_v2 = false;
   std::vector<int64_t> group_tok0, group_pbase, req_dbase;
+  int32_t page_size = 0;
+  int64_t prefix_pages = 0, distinct_pages = 0;  // paged: page-table lengths
   int64_t num_tokens = 0, prefix_keys = 0, distinct_keys = 0;
   // workspace layout (byte offsets)
   size_t off_ctrl = 0, off_cnt = 0, off_items = 0, off_units = 0, off_contribs = 0;
@@ -144,8 +146,17 @@ psa_status psa_plan_create(const psa_problem* prob, const psa_plan_opts* opts, p
     o.tile_pair = 1;
     o.fuse_own = 1;
   }
+  const int32_t ps = prob->page_size;
+  if (ps != 0) {
+    if (ps != 16 && ps != 32 && ps != 64)
+      return fail(PSA_INVALID_ARGUMENT, "page_size must be 0 (packed), 16, 32 or 64");
+    if (!v2)
+      return fail(PSA_UNSUPPORTED,
+                  "paged KV needs the v2 kernel (bf16/f16, head_dim == value_dim == 128)");
+  }
   psa_plan* pl = new (std::nothrow) psa_plan();
   if (!pl) return fail(PSA_INVALID_ARGUMENT, "out of host memory");
+  pl->page_size = ps;
   pl->dims = dims_of(prob);
   std::string err = psa::build_plan(pl->dims, o, &pl->plan);
   if (!err.empty()) {
@@ -164,11 +175,22 @@ psa_status psa_plan_create(const psa_problem* prob, const psa_plan_opts* opts, p
   pl->group_tok0.resize(in.G);
   pl->group_pbase.resize(in.G);
   pl->req_dbase.resize(in.R);
+  // segment bases: packed key offsets, or (paged) offsets into the page tables
+  int64_t pages = 0;
   for (int32_t g = 0; g < in.G; ++g) {
     pl->group_tok0[g] = in.cu_q[in.cu_req[g]];
-    pl->group_pbase[g] = in.cu_prefix[g];
+    const int64_t P = in.cu_prefix[g + 1] - in.cu_prefix[g];
+    pl->group_pbase[g] = ps ? pages : in.cu_prefix[g];
+    if (ps) pages += (P + ps - 1) / ps;
   }
-  for (int32_t r = 0; r < in.R; ++r) pl->req_dbase[r] = in.cu_distinct[r];
+  pl->prefix_pages = pages;
+  pages = 0;
+  for (int32_t r = 0; r < in.R; ++r) {
+    const int64_t D = in.cu_distinct[r + 1] - in.cu_distinct[r];
+    pl->req_dbase[r] = ps ? pages : in.cu_distinct[r];
+    if (ps) pages += (D + ps - 1) / ps;
+  }
+  pl->distinct_pages = pages;
   pl->num_tokens = in.cu_q[in.R];
   pl->prefix_keys = in.cu_prefix[in.G];
   pl->distinct_keys = in.cu_distinct[in.R];
@@ -238,8 +260,29 @@ psa_status psa_run(const psa_problem* prob, const psa_plan* pl, void* ws, size_t
   if (!prob->q || !prob->out) return fail(PSA_INVALID_ARGUMENT, "q/out must not be NULL");
   if ((prob->flags & PSA_FLAG_PARTIAL_OUT) && (!prob->m_out || !prob->l_out))
     return fail(PSA_INVALID_ARGUMENT, "partial output needs m_out and l_out");
+  if (prob->page_size != pl->page_size)
+    return fail(PSA_INVALID_ARGUMENT, "page_size does not match the plan");
+  int64_t prefix_rows = pl->prefix_keys, distinct_rows = pl->distinct_keys;
+  if (pl->page_size) {
+    if ((pl->prefix_pages && !prob->prefix_pages) || (pl->distinct_pages && !prob->distinct_pages))
+      return fail(PSA_INVALID_ARGUMENT, "paged KV needs prefix_pages / distinct_pages");
+    prefix_rows = prob->prefix_cache_rows;
+    distinct_rows = prob->distinct_cache_rows;
+    if (prefix_rows < 0 || distinct_rows < 0 || prefix_rows % pl->page_size ||
+        distinct_rows % pl->page_size || prefix_rows >= (int64_t(1) << 31) ||
+        distinct_rows >= (int64_t(1) << 31))
+      return fail(PSA_INVALID_ARGUMENT,
+                  "cache rows must be non-negative multiples of page_size below 2^31");
+    if ((pl->prefix_pages && prefix_rows == 0) || (pl->distinct_pages && distinct_rows == 0))
+      return fail(PSA_INVALID_ARGUMENT, "empty page cache for a non-empty segment");
+  }
   char* base = static_cast<char*>(ws);
   psa::KParams k{};
+  k.page_size = pl->page_size;
+  k.prefix_pages = prob->prefix_pages;
+  k.distinct_pages = prob->distinct_pages;
+  k.prefix_cache_rows = int32_t(prefix_rows);
+  k.distinct_cache_rows = int32_t(distinct_rows);
   k.q = prob->q; k.kp = prob->k_prefix; k.vp = prob->v_prefix;
   k.kd = prob->k_distinct; k.vd = prob->v_distinct;
   k.out = prob->out; k.lse = prob->lse; k.m_out = prob->m_out; k.l_out = prob->l_out;
@@ -284,7 +327,7 @@ psa_status psa_run(const psa_problem* prob, const psa_plan* pl, void* ws, size_t
                             reinterpret_cast<uintptr_t>(prob->k_distinct) |
                             reinterpret_cast<uintptr_t>(prob->v_distinct);
     if (align & 15) return fail(PSA_INVALID_ARGUMENT, "TMA paths need 16-byte aligned buffers");
-    int te = psa::encode_tile_maps(k, in.dtype, pl->num_tokens, pl->prefix_keys, pl->distinct_keys);
+    int te = psa::encode_tile_maps(k, in.dtype, pl->num_tokens, prefix_rows, distinct_rows);
     if (te != 0) return cuda_fail(te, "cuTensorMapEncodeTiled");
   }
   int e = psa::launch_psa(k, in.dtype, pl->num_sms, pl->ctas_per_sm, pl->use_tiles, stream);

@@ -23,6 +23,38 @@
 #include "psa_device.cuh"
 
 namespace psa {
+
+// One K or V block of `rows` keys (two 64-column chunks, SW128 K-major in `dst`) of
+// a segment: the packed layout (one box per chunk at cache row base + key) or a
+// paged cache (one box per page; page p of the segment is table[base + p]; pages at
+// or past key_end load the all-out-of-bounds row, i.e. zeros). Issued by one lane.
+__device__ __forceinline__ void load_kv_block(const KParams& p, uint8_t* dst, const CUtensorMap* m,
+                                              uint64_t* bar, int h, bool prefix, int64_t base,
+                                              int key, int key_end, int rows) {
+  if (p.page_size == 0) {
+    dev::tma_load_3d(dst, m, bar, 0, h, int(base + key));
+    dev::tma_load_3d(dst + rows * 128, m, bar, 64, h, int(base + key));
+    return;
+  }
+  const int ps = p.page_size;
+  const int32_t* tab = prefix ? p.prefix_pages : p.distinct_pages;
+  const int oob = prefix ? p.prefix_cache_rows : p.distinct_cache_rows;
+  const int np = rows / ps;
+  int prow[8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    const int lk = key + i * ps;
+    prow[i] = (i < np && lk < key_end) ? __ldg(tab + base + lk / ps) * ps : oob;
+  }
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    if (i < np) {
+      dev::tma_load_3d(dst + i * ps * 128, m, bar, 0, h, prow[i]);
+      dev::tma_load_3d(dst + (rows + i * ps) * 128, m, bar, 64, h, prow[i]);
+    }
+  }
+}
+
 namespace dec {
 
 constexpr int kBK = 128;               // keys per block (MMA M)
@@ -246,22 +278,23 @@ __device__ void run(const KParams& p, uint8_t* smem_raw, Shared* sh, uint32_t tm
         } else {
           dev::mbar_arrive(&sh->item_full[q]);
         }
-        int nbA, nb;
-        int64_t pbase, dbase;
-        item_blocks(p, it, nbA, nb, pbase, dbase);
+        const int nbA = (it.pk1 - it.pk0 + kBK - 1) / kBK;
+        const int nb = nbA + (it.dk1 - it.dk0 + kBK - 1) / kBK;
+        const int64_t gbase = nbA ? __ldg(p.group_pbase + it.g) : 0;
+        const int64_t rbase = (it.req >= 0 && it.dk1 > it.dk0) ? __ldg(p.req_dbase + it.req) : 0;
         for (int j = 0; j < nb; ++j) {
-          const CUtensorMap *km, *vm;
-          int key;
-          if (j < nbA) { km = &p.tmd_kp; vm = &p.tmd_vp; key = int(pbase + j * kBK); }
-          else { km = &p.tmd_kd; vm = &p.tmd_vd; key = int(dbase + (j - nbA) * kBK); }
+          const bool pre = j < nbA;
+          const CUtensorMap* km = pre ? &p.tmd_kp : &p.tmd_kd;
+          const CUtensorMap* vm = pre ? &p.tmd_vp : &p.tmd_vd;
+          const int key = pre ? it.pk0 + j * kBK : it.dk0 + (j - nbA) * kBK;
+          const int end = pre ? it.pk1 : it.dk1;
           for (int w = 0; w < 2; ++w, ++c) {  // K then V
             const uint32_t s = c % NSL;
             dev::mbar_wait(&sh->slot_empty[s], ((c / NSL) & 1) ^ 1);
             dbg(p, w, c >> 1);
             dev::mbar_arrive_expect_tx(&sh->slot_full[s], kSlotBytes);
-            const CUtensorMap* m = w == 0 ? km : vm;
-            dev::tma_load_3d(G.slot(s), m, &sh->slot_full[s], 0, it.h, key);
-            dev::tma_load_3d(G.slot(s) + kBK * 128, m, &sh->slot_full[s], 64, it.h, key);
+            load_kv_block(p, G.slot(s), w == 0 ? km : vm, &sh->slot_full[s], it.h, pre,
+                          pre ? gbase : rbase, key, end, kBK);
           }
         }
       }

@@ -1407,10 +1407,11 @@ int encode_tile_maps(KParams& p, int32_t dtype, int64_t T, int64_t prefix_keys,
       if (r != CUDA_SUCCESS) return int(cudaErrorInvalidValue);
       p.dec_q_tma = 1;
     }
-    e = encode_kv(&p.tmd_kp, dt, p.kp, prefix_keys, p.Hkv, p.d, 64, dec::kBK, true);
-    if (!e) e = encode_kv(&p.tmd_vp, dt, p.vp, prefix_keys, p.Hkv, p.dv, 64, dec::kBK, true);
-    if (!e) e = encode_kv(&p.tmd_kd, dt, p.kd, distinct_keys, p.Hkv, p.d, 64, dec::kBK, true);
-    if (!e) e = encode_kv(&p.tmd_vd, dt, p.vd, distinct_keys, p.Hkv, p.dv, 64, dec::kBK, true);
+    const int rows = p.page_size ? p.page_size : dec::kBK;  // paged: one box per page
+    e = encode_kv(&p.tmd_kp, dt, p.kp, prefix_keys, p.Hkv, p.d, 64, rows, true);
+    if (!e) e = encode_kv(&p.tmd_vp, dt, p.vp, prefix_keys, p.Hkv, p.dv, 64, rows, true);
+    if (!e) e = encode_kv(&p.tmd_kd, dt, p.kd, distinct_keys, p.Hkv, p.d, 64, rows, true);
+    if (!e) e = encode_kv(&p.tmd_vd, dt, p.vd, distinct_keys, p.Hkv, p.dv, 64, rows, true);
   }
   if (!e && p.use_vec_fast) {
     e = encode_kv(&p.tmv_kp, dt, p.kp, prefix_keys, p.Hkv, p.d, p.d, vec::kKB, false);

@@ -181,25 +181,30 @@ __device__ __forceinline__ void exp2_poly2(float& y0, float& y1, float x0, float
 struct Block {
   const CUtensorMap* km;
   const CUtensorMap* vm;
-  int key;
-  int nvalid;
+  bool prefix;
+  int64_t base;  // segment base: packed key offset, or page-table offset (paged)
+  int key;       // first key of the block within the segment
+  int end;       // end of the item's keys within the segment
 };
 
 template <typename ItemT>
 __device__ __forceinline__ Block block_at(const KParams& p, const ItemT& it, int jb, int nbA,
                                           int64_t pbase, int64_t dbase) {
   Block b;
-  if (jb < nbA) {
-    b.km = &p.tmd_kp;  // (64, 1, 128)-key boxes, 128-byte swizzle
+  b.prefix = jb < nbA;
+  if (b.prefix) {
+    b.km = &p.tmd_kp;  // (64, 1, 128)-key boxes (paged: page-row boxes), 128-byte swizzle
     b.vm = &p.tmd_vp;
-    b.key = int(pbase + it.pk0 + jb * kBN);
-    b.nvalid = min(kBN, it.pk1 - it.pk0 - jb * kBN);
+    b.base = pbase;
+    b.key = it.pk0 + jb * kBN;
+    b.end = it.pk1;
   } else {
     const int j = jb - nbA;
     b.km = &p.tmd_kd;
     b.vm = &p.tmd_vd;
-    b.key = int(dbase + it.dk0 + j * kBN);
-    b.nvalid = min(kBN, it.dk1 - it.dk0 - j * kBN);
+    b.base = dbase;
+    b.key = it.dk0 + j * kBN;
+    b.end = it.dk1;
   }
   return b;
 }
@@ -285,10 +290,9 @@ __device__ void run_support(const KParams& p, uint8_t* smem_raw, Shared* sh, uin
             const uint32_t s = c % NR;
             dev::mbar_wait(&sh->ring_empty[s], ((c / NR) & 1) ^ 1);
             dev::mbar_arrive_expect_tx(&sh->ring_full[s], kSlotBytes);
-            const CUtensorMap* m = w == 0 ? b.km : b.vm;
             dbg(p, 7 + w, c >> 1);
-            dev::tma_load_3d(G.slot(s), m, &sh->ring_full[s], 0, it.h, b.key);
-            dev::tma_load_3d(G.slot(s) + kBN * 128, m, &sh->ring_full[s], 64, it.h, b.key);
+            load_kv_block(p, G.slot(s), w == 0 ? b.km : b.vm, &sh->ring_full[s], it.h, b.prefix,
+                          b.base, b.key, b.end, kBN);
           }
         }
       }

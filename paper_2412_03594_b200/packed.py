@@ -86,7 +86,12 @@ class PrefixSharedAttention:
     def __init__(self, cu_req, cu_q, cu_prefix, cu_distinct, num_q_heads: int,
                  num_kv_heads: int, head_dim: int, value_dim: Optional[int] = None,
                  dtype: torch.dtype = torch.bfloat16, device=None,
-                 scale: Optional[float] = None, options: Optional[PlanOptions] = None):
+                 scale: Optional[float] = None, options: Optional[PlanOptions] = None,
+                 page_size: int = 0):
+        """``page_size`` > 0 plans for a paged KV cache (see :meth:`__call__` and
+        include/psa.h): K/V come from page caches through page tables instead of the
+        packed segment layout; the plan (work items, merge units) is the same."""
+        self.page_size = int(page_size)
         self.cu_req, self.cu_q = _i64(cu_req), _i64(cu_q)
         self.cu_prefix, self.cu_distinct = _i64(cu_prefix), _i64(cu_distinct)
         self.G = len(self.cu_req) - 1
@@ -110,6 +115,10 @@ class PrefixSharedAttention:
         self.num_tokens = int(self.cu_q[-1])
         self.num_prefix_keys = int(self.cu_prefix[-1])
         self.num_distinct_keys = int(self.cu_distinct[-1])
+        if self.page_size:
+            ps = self.page_size
+            self.num_prefix_pages = int(sum(-(-int(n) // ps) for n in np.diff(self.cu_prefix)))
+            self.num_distinct_pages = int(sum(-(-int(n) // ps) for n in np.diff(self.cu_distinct)))
         prob = self._problem(flags=0)
         handle = C.c_void_p()
         with torch.cuda.device(self.device):
@@ -151,6 +160,7 @@ class PrefixSharedAttention:
         p.cu_q = self.cu_q.ctypes.data_as(i64p)
         p.cu_prefix = self.cu_prefix.ctypes.data_as(i64p)
         p.cu_distinct = self.cu_distinct.ctypes.data_as(i64p)
+        p.page_size = self.page_size
         return p
 
     def plan_tables(self) -> dict:
@@ -182,15 +192,44 @@ class PrefixSharedAttention:
             raise ValidationError(f"{name} must be a contiguous [{rows}, {heads}, {dim}] tensor, "
                                   f"got {tuple(t.shape)}")
 
+    def _check_pages(self, name, t, n):
+        if n == 0:
+            return
+        if t is None or t.device != self.device or t.dtype != torch.int32 or t.dim() != 1 \
+                or t.numel() != n or not t.is_contiguous():
+            raise ValidationError(f"{name} must be a contiguous int32 [{n}] tensor on {self.device}")
+
     def __call__(self, q, k_prefix, v_prefix, k_distinct, v_distinct, out=None, lse=None,
-                 partial: Optional[tuple] = None, stream: Optional[torch.cuda.Stream] = None):
-        """Run the planned op. Returns ``out`` [T, Hq, dv] (or the partial tuple)."""
+                 partial: Optional[tuple] = None, stream: Optional[torch.cuda.Stream] = None,
+                 prefix_pages: Optional[torch.Tensor] = None,
+                 distinct_pages: Optional[torch.Tensor] = None):
+        """Run the planned op. Returns ``out`` [T, Hq, dv] (or the partial tuple).
+
+        Paged plans (``page_size`` > 0): ``k_prefix``/``v_prefix`` and
+        ``k_distinct``/``v_distinct`` are page caches [rows, Hkv, d|dv] (rows a multiple
+        of page_size; one cache may back both), ``prefix_pages`` lists the cache pages
+        of every group's prefix in group order (ceil(P_g / page_size) each) and
+        ``distinct_pages`` those of every request's distinct KV (int32 on the device)."""
         T = self.num_tokens
         self._check("q", q, T, self.Hq, self.d)
-        self._check("k_prefix", k_prefix, self.num_prefix_keys, self.Hkv, self.d)
-        self._check("v_prefix", v_prefix, self.num_prefix_keys, self.Hkv, self.dv)
-        self._check("k_distinct", k_distinct, self.num_distinct_keys, self.Hkv, self.d)
-        self._check("v_distinct", v_distinct, self.num_distinct_keys, self.Hkv, self.dv)
+        if self.page_size:
+            ps = self.page_size
+            for name, t, dim, n in (("k_prefix", k_prefix, self.d, self.num_prefix_keys),
+                                    ("v_prefix", v_prefix, self.dv, self.num_prefix_keys),
+                                    ("k_distinct", k_distinct, self.d, self.num_distinct_keys),
+                                    ("v_distinct", v_distinct, self.dv, self.num_distinct_keys)):
+                if n and (t is None or t.dim() != 3 or t.shape[0] % ps or t.shape[1] != self.Hkv
+                          or t.shape[2] != dim or t.dtype != self.dtype or t.device != self.device
+                          or not t.is_contiguous()):
+                    raise ValidationError(f"{name} must be a contiguous [pages * {ps}, {self.Hkv}, "
+                                          f"{dim}] {self.dtype} page cache on {self.device}")
+            self._check_pages("prefix_pages", prefix_pages, self.num_prefix_pages)
+            self._check_pages("distinct_pages", distinct_pages, self.num_distinct_pages)
+        else:
+            self._check("k_prefix", k_prefix, self.num_prefix_keys, self.Hkv, self.d)
+            self._check("v_prefix", v_prefix, self.num_prefix_keys, self.Hkv, self.dv)
+            self._check("k_distinct", k_distinct, self.num_distinct_keys, self.Hkv, self.d)
+            self._check("v_distinct", v_distinct, self.num_distinct_keys, self.Hkv, self.dv)
         flags = 0
         m_out = l_out = None
         if partial is not None:
@@ -203,6 +242,15 @@ class PrefixSharedAttention:
         prob.k_distinct, prob.v_distinct = _ptr(k_distinct), _ptr(v_distinct)
         prob.out, prob.lse = _ptr(out), _ptr(lse)
         prob.m_out, prob.l_out = _ptr(m_out), _ptr(l_out)
+        if self.page_size:
+            prob.prefix_pages, prob.distinct_pages = _ptr(prefix_pages), _ptr(distinct_pages)
+            prob.prefix_cache_rows = int(k_prefix.shape[0]) if k_prefix is not None else 0
+            prob.distinct_cache_rows = int(k_distinct.shape[0]) if k_distinct is not None else 0
+            if v_prefix is not None and k_prefix is not None and v_prefix.shape[0] != k_prefix.shape[0]:
+                raise ValidationError("k_prefix and v_prefix caches must have the same rows")
+            if v_distinct is not None and k_distinct is not None and \
+                    v_distinct.shape[0] != k_distinct.shape[0]:
+                raise ValidationError("k_distinct and v_distinct caches must have the same rows")
         s = stream if stream is not None else torch.cuda.current_stream(self.device)
         with torch.cuda.device(self.device):
             st = L.lib().psa_run(C.byref(prob), self._plan, _ptr(self.workspace),

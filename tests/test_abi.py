@@ -33,7 +33,7 @@ def test_library_exports_every_declared_symbol():
 
 def test_abi_version_and_error_channel():
     lib = L.lib()
-    assert lib.psa_abi_version() == 2  # psa_plan_opts.kernel_variant
+    assert lib.psa_abi_version() == 3  # psa_problem paged-KV fields
     # a NULL problem is rejected with INVALID_ARGUMENT and a message, no CUDA needed
     h = ctypes.c_void_p()
     st = lib.psa_plan_create(None, None, ctypes.byref(h))
@@ -43,7 +43,7 @@ def test_abi_version_and_error_channel():
 
 def test_struct_sizes_match_header_layout(tmp_path):
     # psa_problem: 8 int32 + double + 4 offset ptrs + 9 buffer ptrs = 32 + 8 + 104 on LP64
-    assert ctypes.sizeof(L.Problem) == 144
+    assert ctypes.sizeof(L.Problem) == 184
     assert ctypes.sizeof(L.PlanOpts) == 36
     assert ctypes.sizeof(L.PlanView) == 56
     # cross-check against the C compiler's view of include/psa.h
