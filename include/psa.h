@@ -199,6 +199,21 @@ psa_status psa_shard_groups(int32_t num_groups, const int64_t* group_cost, int32
 /* Per-group cost used by psa_shard_groups (same model as the planner). */
 psa_status psa_group_costs(const psa_problem* prob, int64_t* group_cost);
 
+/* Host preprocessing: the reference's prompt grouping
+ *   extract_groups(maximize_reuse(build_tree(workload)))   (prefix_tree.py:107-301)
+ * natively. Prompts are tokens[cu_tokens[r] .. cu_tokens[r+1]) (non-empty, int32 ids);
+ * id_rank[r] orders requests with identical prompts like the reference's sorted()
+ * of their string ids. maximize = 0 skips the first-level enlargement. Outputs
+ * (caller-allocated, R = num_requests): *num_groups = G <= R; group g shares the
+ * first group_prefix_len[g] tokens of each member prompt (0 = singleton: the whole
+ * prompt is the suffix) and its members, in the reference's order, are
+ * members[cu_members[g] .. cu_members[g+1]) (request indices; cu_members has R+1
+ * slots). *saved_tokens (nullable) = sum_g (members - 1) * prefix_len. */
+psa_status psa_prefix_groups(int32_t num_requests, const int64_t* cu_tokens, const int32_t* tokens,
+                             const int32_t* id_rank, int32_t maximize, int32_t* num_groups,
+                             int64_t* group_prefix_len, int32_t* cu_members, int32_t* members,
+                             int64_t* saved_tokens);
+
 #ifdef __cplusplus
 }
 #endif

@@ -79,6 +79,9 @@ SIGNATURES = [
     ("psa_debug_set_trace", C.c_int, [C.c_void_p, C.c_int64]),
     ("psa_shard_groups", C.c_int, [C.c_int32, C.POINTER(C.c_int64), C.c_int32, C.POINTER(C.c_int32)]),
     ("psa_group_costs", C.c_int, [C.POINTER(Problem), C.POINTER(C.c_int64)]),
+    ("psa_prefix_groups", C.c_int, [C.c_int32, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int32,
+                                    C.POINTER(C.c_int32), C.c_void_p, C.c_void_p, C.c_void_p,
+                                    C.POINTER(C.c_int64)]),
 ]
 
 _lib = None

@@ -19,7 +19,7 @@ PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 LIB = os.path.join(PKG, "libpsa.so")
-SOURCES = ["psa_kernel.cu", "psa_api.cpp", "psa_plan.cpp"]
+SOURCES = ["psa_kernel.cu", "psa_api.cpp", "psa_plan.cpp", "psa_prefix.cpp"]
 HEADERS = ["psa_kernel.h", "psa_plan.h", "psa_device.cuh", "psa_tile.cuh", "psa_vec.cuh",
            "psa_dec.cuh", "psa_tile2.cuh"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
