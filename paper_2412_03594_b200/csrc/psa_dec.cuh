@@ -133,7 +133,7 @@ __device__ __forceinline__ void merge_loop(const KParams& p, Shared* sh, MergeUn
 // Diagnostics: clock64 of per-block events of CTA 0's first 64 decode blocks, after
 // the tile events (psa_debug_set_trace). Slot = (16 + event) * 64 + global block.
 __device__ __forceinline__ void dbg(const KParams& p, int ev, uint32_t g) {
-  if (p.trace_cap > 0 && blockIdx.x == 0 && g < 64) {
+  if (p.trace_cap > 0 && int(blockIdx.x) == p.dbg_cta && g < 64) {
     long long t;
     asm volatile("mov.u64 %0, %%clock64;" : "=l"(t));
     p.trace[(int64_t(p.num_items) + 4096) * 4 + (16 + ev) * 64 + g] = t;

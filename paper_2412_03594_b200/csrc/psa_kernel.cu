@@ -1272,6 +1272,8 @@ int launch_v2(const KParams& p_in, int32_t num_sms, void* stream) {
   const int dbg = dbg_env ? std::atoi(dbg_env) : 0;
   p.dec_pipes = (dbg & 1) ? 1 : 2;
   p.tile_pp = (dbg & 32) ? 0 : 1;
+  const char* dbg_cta = std::getenv("PSA_DBG_CTA");
+  p.dbg_cta = dbg_cta ? std::atoi(dbg_cta) : 0;
   if (dbg & 2) p.dec_slots = 2;
   size_t smem = 0;
   if (p.use_tiles) smem = tile2::smem_bytes(p.tile_stages);
