@@ -266,6 +266,19 @@ __device__ void run(const KParams& p, uint8_t* smem_raw, Shared* sh, uint32_t tm
       if (next < n_items) {
         it_next = load_item_at(next);
         tok_next = __ldg(p.group_tok0 + it_next.g);
+        if (p.dec_l2_prefetch && lane == 0 && p.page_size == 0) {
+          // warm L2 with the next item's first K/V block while this item's loads wait
+          // for ring slots (raises the bytes in flight beyond the smem ring)
+          const bool pre = it_next.pk1 > it_next.pk0;
+          const int64_t base = pre ? __ldg(p.group_pbase + it_next.g) + it_next.pk0
+                                   : __ldg(p.req_dbase + it_next.req) + it_next.dk0;
+          const CUtensorMap* km = pre ? &p.tmd_kp : &p.tmd_kd;
+          const CUtensorMap* vm = pre ? &p.tmd_vp : &p.tmd_vd;
+          for (int ch = 0; ch < 2; ++ch) {
+            dev::tma_prefetch_3d(km, ch * 64, it_next.h, int(base));
+            dev::tma_prefetch_3d(vm, ch * 64, it_next.h, int(base));
+          }
+        }
       }
       if (lane == 0) {
         sh->item_idx[q] = idx;

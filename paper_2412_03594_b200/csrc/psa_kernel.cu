@@ -1274,6 +1274,7 @@ int launch_v2(const KParams& p_in, int32_t num_sms, void* stream) {
   p.tile_pp = (dbg & 32) ? 0 : 1;
   const char* dbg_cta = std::getenv("PSA_DBG_CTA");
   p.dbg_cta = dbg_cta ? std::atoi(dbg_cta) : 0;
+  p.dec_l2_prefetch = (dbg & 64) ? 1 : 0;  // PSA_DEBUG bit 6 (experiment)
   if (dbg & 2) p.dec_slots = 2;
   size_t smem = 0;
   if (p.use_tiles) smem = tile2::smem_bytes(p.tile_stages);

@@ -148,7 +148,7 @@ def test_lse_output_matches_oracle():
                     assert abs(lse[tok, hq].item() - ref) < 2e-3
 
 
-@pytest.mark.parametrize("name", ["c1", "c2", "c4"])
+@pytest.mark.parametrize("name", ["c1", "c2", "c3", "c4"])
 def test_bench_config_parity_against_oracle(name):
     """Full-size bench batches; the oracle checks a sample of (group, kv head) pairs."""
     spec = W.config(name)
@@ -191,3 +191,24 @@ def check_sampled_groups(spec, b, out, n_groups=3, n_heads=2, seed=0):
                 got = out[t0:t1, h * gqa:(h + 1) * gqa].double().cpu().numpy()
                 worst = max(worst, assert_close(got.reshape(-1, spec.dv), res[i], spec.dtype))
     return worst
+
+
+@pytest.mark.parametrize("dtype", ["f16", "bf16"])
+def test_v2_kernel_half_precision_mixed_batch(dtype):
+    """The v2 kernel in both 16-bit formats (golden cases cover f16 only at d=64):
+    decode + prefill-chunk requests, two-slot and single-slot tiles, merges."""
+    spec = W.Spec("mixed16", 16, 4, 128, 128, dtype, "normal", [700, 33, 0, 2049],
+                  [[(1, 40), (37, 51), (1, 3), (1, 0)], [(1, 64), (20, 1)], [(3, 17)],
+                   [(1, 300)] * 40 + [(130, 77)]], seed=31)
+    b = W.make_batch(spec, "cuda")
+    op = P.PrefixSharedAttention(b["cu_req"], b["cu_q"], b["cu_prefix"], b["cu_distinct"],
+                                 spec.Hq, spec.Hkv, spec.d, spec.dv, spec.torch_dtype, "cuda")
+    out = op(b["q"], b["k_prefix"], b["v_prefix"], b["k_distinct"], b["v_distinct"])
+    torch.cuda.synchronize()
+    assert op.device_error() == 0
+    host = {k: b[k].double().cpu().numpy() for k in ("q", "k_prefix", "v_prefix", "k_distinct",
+                                                       "v_distinct")}
+    ref = S.packed_attention(host["q"], host["k_prefix"], host["v_prefix"], host["k_distinct"],
+                             host["v_distinct"], b["cu_req"], b["cu_q"], b["cu_prefix"],
+                             b["cu_distinct"], spec.Hq, spec.Hkv)
+    assert_close(out.double().cpu().numpy(), ref, dtype)
