@@ -63,6 +63,12 @@ typedef enum psa_dtype {
 
 /* psa_problem.flags */
 #define PSA_FLAG_PARTIAL_OUT 1u /* write unnormalised (o, m, l) instead of out=o/l */
+/* Causal prefill (extension: the reference has no mask, attention.py:12-13; SURVEY.md
+ * §8(f) row 4). Query token j (0-based) of request r with n_q tokens attends distinct
+ * keys 0 .. D_r - n_q + j (the chunk is the tail of its own KV) and every prefix key;
+ * a request without distinct KV (a prefix chunk) attends prefix keys 0 .. P_g - n_q + j.
+ * Decode tokens (n_q = 1) are unaffected. v2 kernel only (else PSA_UNSUPPORTED). */
+#define PSA_FLAG_CAUSAL 2u
 
 typedef struct psa_problem {
   int32_t num_groups;   /* G >= 1 */

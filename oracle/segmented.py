@@ -198,3 +198,46 @@ def packed_attention(q, kp, vp, kd, vd, cu_req, cu_q, cu_prefix, cu_distinct,
                 t0, t1 = int(cu_q[r]), int(cu_q[r + 1])
                 out[t0:t1, h * gqa:(h + 1) * gqa, :] = res[i].reshape(t1 - t0, gqa, dv)
     return out
+
+
+# --------------------------------------------------------------------------
+# Causal prefill (EXTENSION, no reference counterpart: the reference attends every
+# key, attention.py:12-13). Used only to check PSA_FLAG_CAUSAL (include/psa.h):
+# query token j of request r (n_q tokens) sees distinct keys 0 .. D_r - n_q + j and
+# every prefix key; a request without distinct KV sees prefix keys 0 .. P - n_q + j.
+# --------------------------------------------------------------------------
+
+def packed_attention_causal(q, kp, vp, kd, vd, cu_req, cu_q, cu_prefix, cu_distinct,
+                            num_q_heads: int, num_kv_heads: int, scale=None,
+                            groups: Optional[Sequence[int]] = None) -> np.ndarray:
+    q = np.asarray(q, dtype=np.float64)
+    gqa = num_q_heads // num_kv_heads
+    d = q.shape[-1]
+    s = (1.0 / np.sqrt(d)) if scale is None else scale
+    dv = np.asarray(vp).shape[-1] if np.asarray(vp).size else np.asarray(vd).shape[-1]
+    out = np.zeros((q.shape[0], num_q_heads, dv))
+    G = len(cu_req) - 1
+    for g in (range(G) if groups is None else groups):
+        p0, p1 = int(cu_prefix[g]), int(cu_prefix[g + 1])
+        for r in range(int(cu_req[g]), int(cu_req[g + 1])):
+            t0, t1 = int(cu_q[r]), int(cu_q[r + 1])
+            d0, d1 = int(cu_distinct[r]), int(cu_distinct[r + 1])
+            nq, P, D = t1 - t0, p1 - p0, d1 - d0
+            for h in range(num_kv_heads):
+                K = np.concatenate([np.asarray(kp[p0:p1, h], np.float64),
+                                    np.asarray(kd[d0:d1, h], np.float64)])
+                V = np.concatenate([np.asarray(vp[p0:p1, h], np.float64),
+                                    np.asarray(vd[d0:d1, h], np.float64)])
+                for j in range(nq):
+                    vis = np.zeros(P + D, dtype=bool)
+                    if D > 0:
+                        vis[:P] = True
+                        vis[P:P + D - nq + j + 1] = True
+                    else:
+                        vis[:P - nq + j + 1] = True
+                    Qj = q[t0 + j, h * gqa:(h + 1) * gqa]          # [gqa, d]
+                    z = s * (Qj @ K[vis].T)
+                    z -= z.max(axis=1, keepdims=True)
+                    w = np.exp(z)
+                    out[t0 + j, h * gqa:(h + 1) * gqa] = (w @ V[vis]) / w.sum(axis=1, keepdims=True)
+    return out

@@ -17,6 +17,7 @@ LIB_PATH = os.path.join(_HERE, "libpsa.so")
 PSA_OK, PSA_INVALID_ARGUMENT, PSA_UNSUPPORTED, PSA_CUDA_ERROR = 0, 1, 2, 3
 DTYPE_F32, DTYPE_BF16, DTYPE_F16, DTYPE_F64 = 0, 1, 2, 3
 FLAG_PARTIAL_OUT = 1
+FLAG_CAUSAL = 2  # include/psa.h PSA_FLAG_CAUSAL (extension: causal prefill chunks)
 ABI_VERSION = 2  # include/psa.h PSA_ABI_VERSION
 
 

@@ -140,7 +140,8 @@ def entry_token_rows(kb: KernelBatch, batch) -> np.ndarray:
     return rows
 
 
-def run(kb: KernelBatch, q, k_cache, v_cache, num_kv_heads: int, scale=None, options=None):
+def run(kb: KernelBatch, q, k_cache, v_cache, num_kv_heads: int, scale=None, options=None,
+        causal: bool = False):
     """One paged launch for the batch: q [T, Hq, d] in kernel token order; the
     allocator's block pool as the page cache [num_blocks * block_size, Hkv, d]."""
     import torch
@@ -152,4 +153,5 @@ def run(kb: KernelBatch, q, k_cache, v_cache, num_kv_heads: int, scale=None, opt
     dev = q.device
     pp = torch.as_tensor(kb.prefix_pages, device=dev)
     dp = torch.as_tensor(kb.distinct_pages, device=dev)
-    return op(q, k_cache, v_cache, k_cache, v_cache, prefix_pages=pp, distinct_pages=dp)
+    return op(q, k_cache, v_cache, k_cache, v_cache, prefix_pages=pp, distinct_pages=dp,
+              causal=causal)

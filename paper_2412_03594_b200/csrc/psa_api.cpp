@@ -2,6 +2,7 @@
 // objects, workspace layout and launch. No torch, no exceptions across the ABI.
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
@@ -23,12 +24,13 @@ struct psa_plan {
   bool use_dec = false;
   bool use_v2 = false;
   std::vector<int64_t> group_tok0, group_pbase, req_dbase;
+  std::vector<int32_t> tok_lim;  // causal key limits per token (PSA_FLAG_CAUSAL)
   int32_t page_size = 0;
   int64_t prefix_pages = 0, distinct_pages = 0;  // paged: page-table lengths
   int64_t num_tokens = 0, prefix_keys = 0, distinct_keys = 0;
   // workspace layout (byte offsets)
   size_t off_ctrl = 0, off_cnt = 0, off_items = 0, off_units = 0, off_contribs = 0;
-  size_t off_tok0 = 0, off_pbase = 0, off_dbase = 0, off_wso = 0, off_wsml = 0, total = 0;
+  size_t off_tok0 = 0, off_pbase = 0, off_dbase = 0, off_lim = 0, off_wso = 0, off_wsml = 0, total = 0;
 };
 
 namespace {
@@ -103,6 +105,7 @@ void layout(psa_plan* pl) {
   pl->off_tok0 = take(sizeof(int64_t) * pl->group_tok0.size());
   pl->off_pbase = take(sizeof(int64_t) * pl->group_pbase.size());
   pl->off_dbase = take(sizeof(int64_t) * pl->req_dbase.size());
+  pl->off_lim = take(sizeof(int32_t) * pl->tok_lim.size());
   pl->off_wso = take(acc * size_t(pl->plan.workspace_rows) * pl->dims.dv);
   pl->off_wsml = take(acc * size_t(pl->plan.workspace_rows) * 2);
   pl->total = o;
@@ -191,6 +194,22 @@ psa_status psa_plan_create(const psa_problem* prob, const psa_plan_opts* opts, p
     if (ps) pages += (D + ps - 1) / ps;
   }
   pl->distinct_pages = pages;
+  // causal limits (include/psa.h PSA_FLAG_CAUSAL): last visible prefix / distinct key
+  pl->tok_lim.resize(size_t(in.cu_q[in.R]) * 2);
+  for (int32_t g = 0; g < in.G; ++g) {
+    const int64_t P = in.cu_prefix[g + 1] - in.cu_prefix[g];
+    for (int64_t r = in.cu_req[g]; r < in.cu_req[g + 1]; ++r) {
+      const int64_t nq = in.cu_q[r + 1] - in.cu_q[r];
+      const int64_t D = in.cu_distinct[r + 1] - in.cu_distinct[r];
+      for (int64_t j = 0; j < nq; ++j) {
+        const int64_t t = in.cu_q[r] + j;
+        const int64_t lp = D > 0 ? P - 1 : P - nq + j;
+        const int64_t ld = D - nq + j;
+        pl->tok_lim[size_t(t) * 2] = int32_t(std::max<int64_t>(lp, -1));
+        pl->tok_lim[size_t(t) * 2 + 1] = int32_t(std::max<int64_t>(ld, -1));
+      }
+    }
+  }
   pl->num_tokens = in.cu_q[in.R];
   pl->prefix_keys = in.cu_prefix[in.G];
   pl->distinct_keys = in.cu_distinct[in.R];
@@ -235,6 +254,7 @@ psa_status psa_plan_upload(const psa_plan* pl, void* ws, size_t ws_bytes, void* 
       {pl->off_tok0, pl->group_tok0.data(), pl->group_tok0.size() * 8},
       {pl->off_pbase, pl->group_pbase.data(), pl->group_pbase.size() * 8},
       {pl->off_dbase, pl->req_dbase.data(), pl->req_dbase.size() * 8},
+      {pl->off_lim, pl->tok_lim.data(), pl->tok_lim.size() * 4},
   };
   for (const auto& b : blobs) {
     if (b.n == 0) continue;
@@ -292,6 +312,10 @@ psa_status psa_run(const psa_problem* prob, const psa_plan* pl, void* ws, size_t
   k.group_tok0 = reinterpret_cast<const int64_t*>(base + pl->off_tok0);
   k.group_pbase = reinterpret_cast<const int64_t*>(base + pl->off_pbase);
   k.req_dbase = reinterpret_cast<const int64_t*>(base + pl->off_dbase);
+  k.tok_lim = reinterpret_cast<const int32_t*>(base + pl->off_lim);
+  if ((prob->flags & PSA_FLAG_CAUSAL) && !pl->use_v2)
+    return fail(PSA_UNSUPPORTED,
+                "causal masking needs the v2 kernel (bf16/f16, head_dim == value_dim == 128)");
   k.ws_o = base + pl->off_wso;
   k.ws_ml = base + pl->off_wsml;
   k.unit_cnt = reinterpret_cast<int32_t*>(base + pl->off_cnt);

@@ -449,6 +449,22 @@ __device__ void run(const KParams& p, uint8_t* smem_raw, Shared* sh, uint32_t tm
       float m[kR], lp[kR];
 #pragma unroll
       for (int r = 0; r < kR; ++r) { m[r] = r < R ? -INFINITY : 0.f; lp[r] = 0.f; }
+      // causal prefill (PSA_FLAG_CAUSAL): last visible prefix / distinct key per row
+      const bool causal = p.flags & PSA_FLAG_CAUSAL;
+      int limp[kR], limd[kR];
+#pragma unroll
+      for (int r = 0; r < kR; ++r) { limp[r] = INT_MAX; limd[r] = INT_MAX; }
+      if (causal) {
+        const int64_t tok0 = __ldg(p.group_tok0 + it.g);
+#pragma unroll
+        for (int r = 0; r < kR; ++r) {
+          if (r < R) {
+            const int64_t tok = tok0 + (it.row0 + r) / p.gqa;
+            limp[r] = __ldg(p.tok_lim + tok * 2);
+            limd[r] = __ldg(p.tok_lim + tok * 2 + 1);
+          }
+        }
+      }
       for (int j = 0; j < nb; ++j, ++g) {
         const int nvalid = block_nvalid(it, nbA, j);
         dev::mbar_wait(&sh->s_full, g & 1);
@@ -464,9 +480,11 @@ __device__ void run(const KParams& p, uint8_t* smem_raw, Shared* sh, uint32_t tm
         const bool valid = t < nvalid;
         // block max per row: warp reduce, then across the 4 softmax warps
         float x[kR], v[kR];
+        const int key = (j < nbA ? it.pk0 + j * kBK : it.dk0 + (j - nbA) * kBK) + t;
 #pragma unroll
         for (int r = 0; r < kR; ++r) {
-          x[r] = (valid && r < R) ? __uint_as_float(sr[r]) * sc : -INFINITY;
+          const bool vis = !causal || key <= (j < nbA ? limp[r] : limd[r]);
+          x[r] = (valid && r < R && vis) ? __uint_as_float(sr[r]) * sc : -INFINITY;
           v[r] = x[r];
         }
 #pragma unroll
@@ -495,7 +513,7 @@ __device__ void run(const KParams& p, uint8_t* smem_raw, Shared* sh, uint32_t tm
         float e[kR];
 #pragma unroll
         for (int r = 0; r < kR; ++r) {
-          e[r] = dev::ex2(x[r] - m[r]);
+          e[r] = dev::ex2(x[r] - (m[r] == -INFINITY ? 0.f : m[r]));  // all-masked rows: 0
           lp[r] = lp[r] * alpha[r] + e[r];
         }
         // P^T (single buffer): PV_{g-1} must be done reading it (and O before rescale);

@@ -465,6 +465,14 @@ __device__ void run_softmax(const KParams& p, Shared* sh, uint32_t tmem, LoadIte
         continue;
       }
       float m = -INFINITY, l0 = 0.f, l1 = 0.f;
+      // causal prefill (PSA_FLAG_CAUSAL): last visible prefix / distinct key of this row
+      const bool causal = p.flags & PSA_FLAG_CAUSAL;
+      int limp = INT_MAX, limd = INT_MAX;
+      if (causal && row < slot_rows) {
+        const int64_t tok = __ldg(p.group_tok0 + it.g) + (it.row0 + i * tile_rows + row) / gqa;
+        limp = __ldg(p.tok_lim + tok * 2);
+        limd = __ldg(p.tok_lim + tok * 2 + 1);
+      }
       for (int n = 0; n < nb; ++n, ++nblk) {
         const int nvalid = n < nbA ? min(kBN, it.pk1 - it.pk0 - n * kBN)
                                    : min(kBN, it.dk1 - it.dk0 - (n - nbA) * kBN);
@@ -482,12 +490,17 @@ __device__ void run_softmax(const KParams& p, Shared* sh, uint32_t tmem, LoadIte
         dev::tmem_ld32(tS + 96, r[3]);
         dev::tmem_wait_ld();
         if (ev) dbg(p, 1, nblk);
-        if (nvalid < kBN) {
+        int ncut = nvalid;  // columns >= ncut are masked
+        if (causal) {
+          const int key0 = n < nbA ? it.pk0 + n * kBN : it.dk0 + (n - nbA) * kBN;
+          ncut = min(ncut, max(0, (n < nbA ? limp : limd) - key0 + 1));
+        }
+        if (ncut < kBN) {
 #pragma unroll
           for (int c = 0; c < 4; ++c)
 #pragma unroll
             for (int e = 0; e < 32; ++e)
-              if (c * 32 + e >= nvalid) r[c][e] = 0xff800000u;
+              if (c * 32 + e >= ncut) r[c][e] = 0xff800000u;
         }
         // row max of the raw scores (scale > 0): 8 independent FMNMX3 chains
         float a8[8];
@@ -513,7 +526,7 @@ __device__ void run_softmax(const KParams& p, Shared* sh, uint32_t tmem, LoadIte
         }
         l0 *= alpha;
         l1 *= alpha;
-        const float nm = -m;
+        const float nm = m == -INFINITY ? 0.f : -m;  // a row masked so far: P = 0
         // P = 2^(s*sc - m), packed bf16 pairs into r[c][0..15]; sums in (l0, l1)
 #pragma unroll
         for (int c = 0; c < 4; ++c) {

@@ -202,14 +202,17 @@ class PrefixSharedAttention:
     def __call__(self, q, k_prefix, v_prefix, k_distinct, v_distinct, out=None, lse=None,
                  partial: Optional[tuple] = None, stream: Optional[torch.cuda.Stream] = None,
                  prefix_pages: Optional[torch.Tensor] = None,
-                 distinct_pages: Optional[torch.Tensor] = None):
+                 distinct_pages: Optional[torch.Tensor] = None, causal: bool = False):
         """Run the planned op. Returns ``out`` [T, Hq, dv] (or the partial tuple).
 
         Paged plans (``page_size`` > 0): ``k_prefix``/``v_prefix`` and
         ``k_distinct``/``v_distinct`` are page caches [rows, Hkv, d|dv] (rows a multiple
         of page_size; one cache may back both), ``prefix_pages`` lists the cache pages
         of every group's prefix in group order (ceil(P_g / page_size) each) and
-        ``distinct_pages`` those of every request's distinct KV (int32 on the device)."""
+        ``distinct_pages`` those of every request's distinct KV (int32 on the device).
+
+        ``causal``: prefill-chunk tokens see only keys up to their own position
+        (include/psa.h PSA_FLAG_CAUSAL — an extension; the reference attends every key)."""
         T = self.num_tokens
         self._check("q", q, T, self.Hq, self.d)
         if self.page_size:
@@ -237,6 +240,8 @@ class PrefixSharedAttention:
             out, m_out, l_out = partial
         elif out is None:
             out = torch.empty((T, self.Hq, self.dv), dtype=self.dtype, device=self.device)
+        if causal:
+            flags |= L.FLAG_CAUSAL
         prob = self._problem(flags)
         prob.q, prob.k_prefix, prob.v_prefix = _ptr(q), _ptr(k_prefix), _ptr(v_prefix)
         prob.k_distinct, prob.v_distinct = _ptr(k_distinct), _ptr(v_distinct)
