@@ -202,7 +202,8 @@ struct NoFast {
                          const float (&)[kR], const Other&) const {}
 };
 
-template <typename T, typename LoadItem, typename Finish, typename MergeUnit, typename Fast = NoFast>
+template <typename T, bool kCausal = false, typename LoadItem, typename Finish, typename MergeUnit,
+          typename Fast = NoFast>
 __device__ void run(const KParams& p, uint8_t* smem_raw, Shared* sh, uint32_t tmem, int pi,
                     LoadItem&& load_item_at, Finish&& finish, MergeUnit&& merge_unit,
                     const Fast& fast = Fast()) {
@@ -266,19 +267,6 @@ __device__ void run(const KParams& p, uint8_t* smem_raw, Shared* sh, uint32_t tm
       if (next < n_items) {
         it_next = load_item_at(next);
         tok_next = __ldg(p.group_tok0 + it_next.g);
-        if (p.dec_l2_prefetch && lane == 0 && p.page_size == 0) {
-          // warm L2 with the next item's first K/V block while this item's loads wait
-          // for ring slots (raises the bytes in flight beyond the smem ring)
-          const bool pre = it_next.pk1 > it_next.pk0;
-          const int64_t base = pre ? __ldg(p.group_pbase + it_next.g) + it_next.pk0
-                                   : __ldg(p.req_dbase + it_next.req) + it_next.dk0;
-          const CUtensorMap* km = pre ? &p.tmd_kp : &p.tmd_kd;
-          const CUtensorMap* vm = pre ? &p.tmd_vp : &p.tmd_vd;
-          for (int ch = 0; ch < 2; ++ch) {
-            dev::tma_prefetch_3d(km, ch * 64, it_next.h, int(base));
-            dev::tma_prefetch_3d(vm, ch * 64, it_next.h, int(base));
-          }
-        }
       }
       if (lane == 0) {
         sh->item_idx[q] = idx;
@@ -450,11 +438,11 @@ __device__ void run(const KParams& p, uint8_t* smem_raw, Shared* sh, uint32_t tm
 #pragma unroll
       for (int r = 0; r < kR; ++r) { m[r] = r < R ? -INFINITY : 0.f; lp[r] = 0.f; }
       // causal prefill (PSA_FLAG_CAUSAL): last visible prefix / distinct key per row
-      const bool causal = p.flags & PSA_FLAG_CAUSAL;
+      constexpr bool causal = kCausal;  // a separate kernel: no cost when off
       int limp[kR], limd[kR];
 #pragma unroll
       for (int r = 0; r < kR; ++r) { limp[r] = INT_MAX; limd[r] = INT_MAX; }
-      if (causal) {
+      if constexpr (causal) {
         const int64_t tok0 = __ldg(p.group_tok0 + it.g);
 #pragma unroll
         for (int r = 0; r < kR; ++r) {

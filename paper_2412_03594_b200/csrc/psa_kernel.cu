@@ -1037,7 +1037,7 @@ __device__ __forceinline__ void setmaxnreg_dec_72() { asm volatile("setmaxnreg.d
 __device__ __forceinline__ void setmaxnreg_dec_128() { asm volatile("setmaxnreg.dec.sync.aligned.u32 128;"); }
 __device__ __forceinline__ void setmaxnreg_inc_128() { asm volatile("setmaxnreg.inc.sync.aligned.u32 128;"); }
 
-template <typename T, int kEmu>
+template <typename T, int kEmu, bool kCausal>
 __global__ void __launch_bounds__(kV2Threads, 1) psa_v2(const __grid_constant__ KParams p) {
   extern __shared__ __align__(1024) uint8_t smem[];
   __shared__ tile2::Shared s_t2;
@@ -1114,7 +1114,7 @@ __global__ void __launch_bounds__(kV2Threads, 1) psa_v2(const __grid_constant__ 
   if (p.use_tiles) {
     if (warp < 8) {
       setmaxnreg_inc_184();
-      tile2::run_softmax<T, kEmu>(p, &s_t2, tmem, load_at);
+      tile2::run_softmax<T, kEmu, kCausal>(p, &s_t2, tmem, load_at);
       phase_mark(0);
       setmaxnreg_dec_128();
     } else {
@@ -1140,7 +1140,7 @@ __global__ void __launch_bounds__(kV2Threads, 1) psa_v2(const __grid_constant__ 
                       const float (&L)[dec::kR], const float (&ov)[dec::kR]) {
       dec_finish<T>(p, &s_dec[pi], it, idx, t, R, m, L, ov, pi);
     };
-    dec::run<T>(p, smem + pi * half, &s_dec[pi], tmem + 64u * uint32_t(pi), pi, load_at, finish,
+    dec::run<T, kCausal>(p, smem + pi * half, &s_dec[pi], tmem + 64u * uint32_t(pi), pi, load_at, finish,
                 arrive_dec, DecFast<T>{p});
     // diagnostics: decode-phase record at trace row num_items + 3072 + CTA:
     // {softmax warps, producer, MMA warp, merge warps} done
@@ -1274,16 +1274,13 @@ int launch_v2(const KParams& p_in, int32_t num_sms, void* stream) {
   p.tile_pp = (dbg & 32) ? 0 : 1;
   const char* dbg_cta = std::getenv("PSA_DBG_CTA");
   p.dbg_cta = dbg_cta ? std::atoi(dbg_cta) : 0;
-  p.dec_l2_prefetch = (dbg & 64) ? 1 : 0;  // PSA_DEBUG bit 6 (experiment)
   if (dbg & 2) p.dec_slots = 2;
   size_t smem = 0;
   if (p.use_tiles) smem = tile2::smem_bytes(p.tile_stages);
   if (p.use_dec) {
     smem = std::max(smem, 2 * dec::pipe_stride(p.dec_slots));
   }
-  // PSA_DEBUG bits 2-3 (diagnostics): tile softmax exp emulation every 2nd / 3rd pair
-  auto kern = psa_v2<T, kV2EmuEvery>;
-  if ((dbg >> 2) & 3) kern = ((dbg >> 2) & 3) == 1 ? psa_v2<T, 2> : ((dbg >> 2) & 3) == 2 ? psa_v2<T, 3> : psa_v2<T, 0>;
+  auto kern = (p.flags & PSA_FLAG_CAUSAL) ? psa_v2<T, kV2EmuEvery, true> : psa_v2<T, kV2EmuEvery, false>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        int(smem));
   if (e != cudaSuccess) return e;

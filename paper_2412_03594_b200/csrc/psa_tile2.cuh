@@ -428,7 +428,7 @@ __device__ void run_support(const KParams& p, uint8_t* smem_raw, Shared* sh, uin
   }
 }
 
-template <typename T, int kEmuEvery, typename LoadItem>
+template <typename T, int kEmuEvery, bool kCausal, typename LoadItem>
 __device__ void run_softmax(const KParams& p, Shared* sh, uint32_t tmem, LoadItem&& load_item_at) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int gqa = p.gqa;
@@ -466,7 +466,7 @@ __device__ void run_softmax(const KParams& p, Shared* sh, uint32_t tmem, LoadIte
       }
       float m = -INFINITY, l0 = 0.f, l1 = 0.f;
       // causal prefill (PSA_FLAG_CAUSAL): last visible prefix / distinct key of this row
-      const bool causal = p.flags & PSA_FLAG_CAUSAL;
+      constexpr bool causal = kCausal;  // a separate kernel: no cost when off
       int limp = INT_MAX, limd = INT_MAX;
       if (causal && row < slot_rows) {
         const int64_t tok = __ldg(p.group_tok0 + it.g) + (it.row0 + i * tile_rows + row) / gqa;
@@ -491,7 +491,7 @@ __device__ void run_softmax(const KParams& p, Shared* sh, uint32_t tmem, LoadIte
         dev::tmem_wait_ld();
         if (ev) dbg(p, 1, nblk);
         int ncut = nvalid;  // columns >= ncut are masked
-        if (causal) {
+        if constexpr (causal) {
           const int key0 = n < nbA ? it.pk0 + n * kBN : it.dk0 + (n - nbA) * kBN;
           ncut = min(ncut, max(0, (n < nbA ? limp : limd) - key0 + 1));
         }
