@@ -103,6 +103,15 @@ def lib():
     with _lock:
         if _lib is not None:
             return _lib
+        alt = os.environ.get("PSA_LIB_PATH")  # diagnostics: A/B another build of the library
+        if alt:
+            handle = C.CDLL(alt)
+            for name, res, args in SIGNATURES:
+                fn = getattr(handle, name)
+                fn.restype = res
+                fn.argtypes = args
+            _lib = handle
+            return _lib
         if os.environ.get("PSA_NO_BUILD") != "1":
             try:
                 from . import build as _build
