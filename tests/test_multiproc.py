@@ -127,3 +127,48 @@ def test_bench_rank_specs_weak_and_strong():
         assert scaling == "strong"
         seen += s.group_ids
     assert sorted(seen) == list(range(1024))
+
+
+def _gather_worker(rank, world, port, q):
+    """Each rank runs the float64 oracle on its shard (the kernel's stand-in on CPU) and
+    the gather reassembles the full batch output in global token order."""
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2412_03594_b200 import distributed as D
+        spec = _small_skewed()
+        b = W.make_batch(spec, "cpu")
+        shards = D.shard(b["cu_req"], b["cu_q"], b["cu_prefix"], b["cu_distinct"], spec.Hq,
+                         spec.Hkv, spec.d, spec.dv, spec.torch_dtype, world)
+        s = shards[rank]
+        host = {k: b[k].double().numpy() for k in ("q", "k_prefix", "v_prefix", "k_distinct",
+                                                     "v_distinct")}
+        local = S.packed_attention(host["q"][s.token_rows], host["k_prefix"][s.prefix_rows],
+                                   host["v_prefix"][s.prefix_rows],
+                                   host["k_distinct"][s.distinct_rows],
+                                   host["v_distinct"][s.distinct_rows], s.cu_req, s.cu_q,
+                                   s.cu_prefix, s.cu_distinct, spec.Hq, spec.Hkv)
+        full = D.gather_outputs(torch.as_tensor(local), shards, rank)
+        if rank == 0:
+            ref = S.packed_attention(host["q"], host["k_prefix"], host["v_prefix"],
+                                     host["k_distinct"], host["v_distinct"], b["cu_req"],
+                                     b["cu_q"], b["cu_prefix"], b["cu_distinct"], spec.Hq,
+                                     spec.Hkv)
+            q.put(float(np.abs(full.numpy() - ref).max()))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.timeout(300)
+def test_gloo_world2_shard_run_and_output_gather():
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_gather_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    err = q.get(timeout=240)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    assert err == 0.0
