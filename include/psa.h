@@ -117,7 +117,8 @@ typedef struct psa_problem {
 typedef struct psa_plan_opts {
   int32_t num_sms;        /* 0 = query the current device */
   int32_t ctas_per_sm;    /* 0 = default (2) */
-  int32_t tile_min_rows;  /* stacked rows at which a segment uses tcgen05 tiles (0 = default 32) */
+  int32_t tile_min_rows;  /* stacked rows at which a segment uses tcgen05 tiles (0 = default: 16 for
+                             the v2 kernel, 32 otherwise) */
   int32_t disable_tiles;  /* 1 = every item on the CUDA-core path (diagnostics) */
   int32_t min_chunk_keys; /* tile items: minimum KV chunk, 0 = default (512) */
   int32_t max_chunk_keys; /* 0 = default (16384) */

@@ -49,6 +49,9 @@ def tiles_supported(dtype, d, dv, Hq, Hkv, disable_tiles=0):
     return Hq // Hkv <= TILE_M
 
 
+V2_TILE_MIN_ROWS = 16  # psa_plan_create's default tile threshold for the v2 kernel
+
+
 def v2_selected(dtype, d, dv, disable_vec_fast=0, kernel_variant=0):
     """psa_plan_create's kernel choice: the v2 kernel (tile_pair, fuse_own, one CTA
     per SM) for bf16/f16 with d == dv == 128 unless a diagnostic option opts out."""

@@ -148,6 +148,9 @@ psa_status psa_plan_create(const psa_problem* prob, const psa_plan_opts* opts, p
     o.ctas_per_sm = 1;
     o.tile_pair = 1;
     o.fuse_own = 1;
+    // ping-pong tiles beat the decode pipeline from 16 stacked rows on (c4: prefixes
+    // of small groups are read once instead of once per 8-row VEC item)
+    if (!opts || opts->tile_min_rows <= 0) o.tile_min_rows = 16;
   }
   const int32_t ps = prob->page_size;
   if (ps != 0) {

@@ -31,7 +31,7 @@ def _compare(off, Hq, Hkv, d, dv, dt, **opt):
                          off["cu_req"], off["cu_q"], off["cu_prefix"], off["cu_distinct"],
                          num_sms=opts.num_sms, ctas_per_sm=1 if v2 else (opts.ctas_per_sm or 2),
                          tile_pair=int(v2), fuse_own=int(v2),
-                         tile_min_rows=opts.tile_min_rows or 32,
+                         tile_min_rows=opts.tile_min_rows or (OP.V2_TILE_MIN_ROWS if v2 else 32),
                          disable_tiles=opts.disable_tiles,
                          min_chunk_keys=opts.min_chunk_keys or 512,
                          max_chunk_keys=opts.max_chunk_keys or 16384,
