@@ -1275,10 +1275,14 @@ int launch_v2(const KParams& p_in, int32_t num_sms, void* stream) {
   const char* dbg_cta = std::getenv("PSA_DBG_CTA");
   p.dbg_cta = dbg_cta ? std::atoi(dbg_cta) : 0;
   if (dbg & 2) p.dec_slots = 2;
+  if (dbg & 128) {  // one decode pipeline with the whole ring (diagnostics)
+    p.dec_pipes = 1;
+    while (p.dec_slots < dec::kMaxSlots && dec::pipe_stride(p.dec_slots + 1) <= budget) ++p.dec_slots;
+  }
   size_t smem = 0;
   if (p.use_tiles) smem = tile2::smem_bytes(p.tile_stages);
   if (p.use_dec) {
-    smem = std::max(smem, 2 * dec::pipe_stride(p.dec_slots));
+    smem = std::max(smem, size_t(p.dec_pipes) * dec::pipe_stride(p.dec_slots));
   }
   auto kern = (p.flags & PSA_FLAG_CAUSAL) ? psa_v2<T, kV2EmuEvery, true> : psa_v2<T, kV2EmuEvery, false>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
