@@ -349,6 +349,12 @@ def main():
                    "plan_items": op.num_items},
         "tflops": round(achieved_tflops * world, 2), "hbm_gbs": round(achieved_gbs * world, 1),
         "t_roof_us": round(t_roof * 1e6, 2),
+        # BASELINE.json's literal split: the slower of the prefix FLOP at tensor peak and
+        # the distinct KV bytes at HBM bandwidth (ignores prefix KV, Q and O traffic)
+        "t_roof_split_us": round(max(cost["flops_prefix"] / (tc_peak * 1e12),
+                                     cost["bytes_distinct"] / (hbm_peak * 1e9)) * 1e6, 2),
+        "frac_split": round(max(cost["flops_prefix"] / (tc_peak * 1e12),
+                                cost["bytes_distinct"] / (hbm_peak * 1e9)) / (ms_rank * 1e-3), 4),
         "roofline": {"bound": bound, "achieved": round(achieved, 2), "peak": peak, "unit": unit,
                      "frac": round(achieved / peak, 4), "traffic": traffic,
                      "peak_source": peaks_src, "t_roof_over_t": round(t_roof / (ms_rank * 1e-3), 4),
