@@ -1032,8 +1032,8 @@ __global__ void __launch_bounds__(kThreads, 2) psa_persistent(const __grid_const
 constexpr int kV2Threads = 512;
 constexpr int kV2EmuEvery = 4;  // every 4th exp pair of the tile softmax on the FMA pipe
 
-__device__ __forceinline__ void setmaxnreg_inc_176() { asm volatile("setmaxnreg.inc.sync.aligned.u32 176;"); }
-__device__ __forceinline__ void setmaxnreg_dec_80() { asm volatile("setmaxnreg.dec.sync.aligned.u32 80;"); }
+__device__ __forceinline__ void setmaxnreg_inc_168() { asm volatile("setmaxnreg.inc.sync.aligned.u32 168;"); }
+__device__ __forceinline__ void setmaxnreg_dec_88() { asm volatile("setmaxnreg.dec.sync.aligned.u32 88;"); }
 __device__ __forceinline__ void setmaxnreg_dec_128() { asm volatile("setmaxnreg.dec.sync.aligned.u32 128;"); }
 __device__ __forceinline__ void setmaxnreg_inc_128() { asm volatile("setmaxnreg.inc.sync.aligned.u32 128;"); }
 
@@ -1113,12 +1113,12 @@ __global__ void __launch_bounds__(kV2Threads, 1) psa_v2(const __grid_constant__ 
   };
   if (p.use_tiles) {
     if (warp < 8) {
-      setmaxnreg_inc_176();
+      setmaxnreg_inc_168();
       tile2::run_softmax<T, kEmu, kCausal>(p, &s_t2, tmem, load_at);
       phase_mark(0);
       setmaxnreg_dec_128();
     } else {
-      setmaxnreg_dec_80();
+      setmaxnreg_dec_88();
       if (warp >= tile2::kMergeWarp0) {
         dev::mq_drain(&s_t2.mq, 2, tile_task);
         phase_mark(2);
