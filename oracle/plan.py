@@ -153,7 +153,8 @@ def build_plan(G, R, Hq, Hkv, d, dv, dtype, cu_req, cu_q, cu_prefix, cu_distinct
                 lo = mid + CHUNK_ALIGN
         lo = lo if tile_items(lo) <= tile_target else hi
     chunk = lo
-    vchunk = _cdiv(total_vec * Hkv, vec_ctas * VEC_WARPS * VEC_WAVES)
+    vec_consumers = vec_ctas * VEC_WAVES if tile_pair else vec_ctas * VEC_WARPS * VEC_WAVES
+    vchunk = _cdiv(total_vec * Hkv, vec_consumers)
     vchunk = _rup(min(max(vchunk, CHUNK_ALIGN), VEC_MAX_KEYS), CHUNK_ALIGN)
 
     def per(L, kind):

@@ -179,7 +179,10 @@ std::string build_plan(const PlanInput& in, const PlanOptions& opt, Plan* out) {
     lo = tile_items(lo) <= tile_target ? lo : hi;
   }
   const int64_t chunk = lo;
-  int64_t vchunk = ceil_div(total_vec, vec_ctas * kVecWarps * kVecWaves);
+  // consumers: every warp of the legacy kernel; the v2 kernel's decode pipelines
+  // (two per CTA) each take whole items
+  const int64_t vec_consumers = opt.tile_pair ? vec_ctas * kVecWaves : vec_ctas * kVecWarps * kVecWaves;
+  int64_t vchunk = ceil_div(total_vec, vec_consumers);
   vchunk = std::min<int64_t>(std::max<int64_t>(vchunk, kChunkAlign), kVecMaxKeys);
   vchunk = round_up(vchunk, kChunkAlign);
   const Chunking ck{chunk};

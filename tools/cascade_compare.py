@@ -36,16 +36,46 @@ def timeit(fn, iters=50):
     return e0.elapsed_time(e1) / iters * 1e3
 
 
+def fig9_specs():
+    """Kernel-comparison shapes in the style of the paper's Fig. 9:
+    setting P/D/k = shared-prefix length / distinct length / requests per prefix group,
+    decoding with 32 and 256 requests, and chunked prefill (7 prefill chunks of 512
+    tokens with 512 own keys, plus 256 decoding requests). Llama-3-8B heads, bf16."""
+    out = []
+    for R in (32, 256):
+        for P, D in ((256, 2048), (2048, 256), (2048, 2048), (8192, 256)):
+            for k in (R, 16, 4):
+                G = R // k
+                out.append((f"dec{R}_{P}/{D}/{'all' if k == R else k}",
+                            W.Spec("fig9", 32, 8, 128, 128, "bf16", "normal", [P] * G,
+                                   [[(1, D)] * k for _ in range(G)], seed=9)))
+    for P, k in ((2048, 32), (2048, 263)):
+        G = 263 // k if k < 263 else 1
+        reqs = [[(1, 256)] * k for _ in range(G)]
+        for i in range(7):  # prefill chunks spread over the groups
+            reqs[i % G].append((512, 512))
+        out.append((f"chunked7+256_{P}/256/{k}",
+                    W.Spec("fig9", 32, 8, 128, 128, "bf16", "normal", [P] * G, reqs, seed=9)))
+    return out
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--config", default="c2")
     ap.add_argument("--page", type=int, default=16)
+    ap.add_argument("--fig9", action="store_true", help="sweep the Fig. 9-style shapes")
     args = ap.parse_args()
+    if args.fig9:
+        for name, spec in fig9_specs():
+            compare(spec, name, args.page)
+        return
+    compare(W.config(args.config), args.config, args.page)
+
+
+def compare(spec, name, ps):
     import flashinfer
-    spec = W.config(args.config)
     b = W.make_batch(spec, "cuda")
     off = W.offsets(spec)
-    ps = args.page
     # ours (packed layout)
     op = P.PrefixSharedAttention(off["cu_req"], off["cu_q"], off["cu_prefix"], off["cu_distinct"],
                                  spec.Hq, spec.Hkv, spec.d, spec.dv, spec.torch_dtype, "cuda")
@@ -80,10 +110,10 @@ def main():
     fi_out = wrapper.run(b["q"], cache)
     fi_us = timeit(lambda: wrapper.run(b["q"], cache))
     diff = float((fi_out.float() - out.float()).abs().max())
-    print(json.dumps({"config": args.config, "page_size": ps, "ours_us": round(ours_us, 1),
+    print(json.dumps({"config": name, "page_size": ps, "ours_us": round(ours_us, 1),
                       "flashinfer_cascade_us": round(fi_us, 1),
                       "speedup": round(fi_us / ours_us, 2), "max_abs_diff": diff,
-                      "flashinfer": flashinfer.__version__}))
+                      "flashinfer": flashinfer.__version__}), flush=True)
 
 
 if __name__ == "__main__":
