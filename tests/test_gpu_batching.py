@@ -46,3 +46,27 @@ def test_token_batch_paged_launch(i):
     ref = S.packed_attention(h["q"], h["kp"], h["vp"], h["kd"], h["vd"], kb.cu_req, kb.cu_q,
                              kb.cu_prefix, kb.cu_distinct, HQ, HKV)
     assert float(np.abs(out.double().cpu().numpy() - ref).max()) <= 2e-2
+
+
+@pytest.mark.parametrize("i", [2, 5, 9])
+def test_token_batch_paged_causal_launch(i):
+    """The same recorded scheduler batches with causal prefill (an extension): paged +
+    causal kernel against the causal float64 oracle on the gathered KV."""
+    bs, nblk = int(FIX["block_size"]), int(FIX["total_blocks"])
+    kb = B.KernelBatch(bs, *(FIX[f"b{i}_{k}"] for k in (
+        "cu_req", "cu_q", "cu_prefix", "cu_distinct", "prefix_pages", "distinct_pages",
+        "token_entry", "token_offset", "request_entry")))
+    gen = torch.Generator(device="cuda").manual_seed(300 + i)
+    k_cache = torch.randn((nblk * bs, HKV, D), generator=gen, device="cuda").to(torch.bfloat16)
+    v_cache = torch.randn((nblk * bs, HKV, D), generator=gen, device="cuda").to(torch.bfloat16)
+    q = torch.randn((kb.num_tokens, HQ, D), generator=gen, device="cuda").to(torch.bfloat16)
+    out = B.run(kb, q, k_cache, v_cache, HKV, causal=True)
+    torch.cuda.synchronize()
+    pr = torch.as_tensor(PG.physical_rows(np.diff(kb.cu_prefix), kb.prefix_pages, bs), device="cuda")
+    dr = torch.as_tensor(PG.physical_rows(np.diff(kb.cu_distinct), kb.distinct_pages, bs),
+                         device="cuda")
+    h = {k: t.double().cpu().numpy() for k, t in dict(
+        q=q, kp=k_cache[pr], vp=v_cache[pr], kd=k_cache[dr], vd=v_cache[dr]).items()}
+    ref = S.packed_attention_causal(h["q"], h["kp"], h["vp"], h["kd"], h["vd"], kb.cu_req,
+                                    kb.cu_q, kb.cu_prefix, kb.cu_distinct, HQ, HKV)
+    assert float(np.abs(out.double().cpu().numpy() - ref).max()) <= 2e-2
