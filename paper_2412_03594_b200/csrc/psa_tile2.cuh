@@ -465,6 +465,7 @@ __device__ void run_softmax(const KParams& p, Shared* sh, uint32_t tmem, LoadIte
         continue;
       }
       float m = -INFINITY, l0 = 0.f, l1 = 0.f;
+      const bool warp_rows = (warp & 3) * 32 < slot_rows;  // this warp has a valid row
       // causal prefill (PSA_FLAG_CAUSAL): last visible prefix / distinct key of this row
       constexpr bool causal = kCausal;  // a separate kernel: no cost when off
       int limp = INT_MAX, limd = INT_MAX;
@@ -479,6 +480,14 @@ __device__ void run_softmax(const KParams& p, Shared* sh, uint32_t tmem, LoadIte
         const int b = pp ? (n & 1) : i;  // S buffer of this block
         dev::mbar_wait(&sh->s_full[b], hs[b] & 1);
         ++hs[b];
+        if (!warp_rows) {
+          // every row of this warp is past the slot's rows (small groups): keep the
+          // barrier pace (one p_full arrival per block, after this block's S) and skip
+          // the softmax — its P rows feed only output rows that are never written
+          __syncwarp();
+          if (lane == 0) dev::mbar_arrive(&sh->p_full[b]);
+          continue;
+        }
         const uint32_t tS = tmem + uint32_t(b) * 128 + lane_base;
         const bool ev = threadIdx.x == 0;
         if (ev) dbg(p, 0, nblk);
