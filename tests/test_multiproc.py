@@ -172,3 +172,24 @@ def test_gloo_world2_shard_run_and_output_gather():
         p.join(timeout=60)
         assert p.exitcode == 0
     assert err == 0.0
+
+
+def test_shard_edge_cases_on_host():
+    """More ranks than groups (empty shards), one rank, and token/key row maps that
+    tile the batch exactly once (no GPU: the planner's cost model is host code)."""
+    from paper_2412_03594_b200 import distributed as D
+    spec = _small_skewed()
+    off = W.offsets(spec)
+    for world in (1, 3, spec.G + 2):
+        shards = D.shard(off["cu_req"], off["cu_q"], off["cu_prefix"], off["cu_distinct"],
+                         spec.Hq, spec.Hkv, spec.d, spec.dv, spec.torch_dtype, world)
+        assert len(shards) == world
+        assert sorted(g for s in shards for g in s.groups.tolist()) == list(range(spec.G))
+        for name, total in (("token_rows", off["cu_q"][-1]), ("prefix_rows", off["cu_prefix"][-1]),
+                            ("distinct_rows", off["cu_distinct"][-1])):
+            rows = np.concatenate([getattr(s, name) for s in shards])
+            assert sorted(rows.tolist()) == list(range(int(total)))
+        for s in shards:
+            assert s.cu_q[-1] == len(s.token_rows) and s.cu_prefix[-1] == len(s.prefix_rows)
+            assert s.cu_distinct[-1] == len(s.distinct_rows)
+            assert len(s.cu_req) == len(s.groups) + 1
