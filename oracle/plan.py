@@ -248,8 +248,16 @@ def build_plan(G, R, Hq, Hkv, d, dv, dtype, cu_req, cu_q, cu_prefix, cu_distinct
         else:
             cost.append(max(nbytes * BYTE_WEIGHT,
                             2 * _rup(it[IT_ROWS], 4) * keys * width * VEC_FLOP_WEIGHT))
-    # TILE items first (CTA-level queue), then VEC items; each by cost descending
-    order = sorted(range(len(items)), key=lambda i: (items[i][IT_KIND] != KIND_TILE, -cost[i]))
+    # TILE items first (CTA-level queue), then VEC items; each by cost descending.
+    # Equal-cost VEC items: the kv heads of one (request, key chunk) side by side
+    # (psa_plan.cpp build_plan step 4).
+    def _key(i):
+        it = items[i]
+        if it[IT_KIND] == KIND_TILE:
+            return (False, -cost[i], ())
+        return (True, -cost[i], (it[IT_GROUP], it[IT_REQUEST], it[IT_ROW0], it[IT_PK0],
+                                 it[IT_DK0], it[IT_HEAD]))
+    order = sorted(range(len(items)), key=_key)
     return dict(
         items=np.array([items[i] for i in order], dtype=np.int32).reshape(-1, ITEM_WORDS),
         units=np.array(units, dtype=np.int32).reshape(-1, UNIT_WORDS),

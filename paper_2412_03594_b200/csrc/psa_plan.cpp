@@ -285,7 +285,8 @@ std::string build_plan(const PlanInput& in, const PlanOptions& opt, Plan* out) {
     }
   }
 
-  // 4. LPT queue order: cost descending, canonical index ascending.
+  // 4. LPT queue order: cost descending; ties: tiles by canonical index, VEC items
+  //    heads-fastest (below).
   std::vector<int64_t> cost(items.size());
   for (size_t i = 0; i < items.size(); ++i) {
     const auto& it = items[i];
@@ -299,13 +300,21 @@ std::string build_plan(const PlanInput& in, const PlanOptions& opt, Plan* out) {
     }
   }
   // Queue order: TILE items first (CTA-level queue), then VEC items (warp-level
-  // queue); each by cost descending, canonical index ascending.
+  // queue); each by cost descending.
   std::vector<int32_t> order(items.size());
   std::iota(order.begin(), order.end(), 0);
   std::stable_sort(order.begin(), order.end(), [&](int32_t a, int32_t b) {
     const bool ta = items[a][kItKind] == kItemTile, tb = items[b][kItKind] == kItemTile;
     if (ta != tb) return ta;
-    return cost[a] > cost[b];
+    if (cost[a] != cost[b]) return cost[a] > cost[b];
+    if (ta) return false;
+    // equal-cost VEC items: the kv heads of one (request, key chunk) side by side, so
+    // the pipelines running at the same time read whole token rows of the cache
+    const auto& x = items[a];
+    const auto& y = items[b];
+    const std::array<int32_t, 6> kx{x[kItGroup], x[kItRequest], x[kItRow0], x[kItPk0], x[kItDk0], x[kItHead]};
+    const std::array<int32_t, 6> ky{y[kItGroup], y[kItRequest], y[kItRow0], y[kItPk0], y[kItDk0], y[kItHead]};
+    return kx < ky;
   });
   out->tile_cost = out->total_cost = 0;
   for (size_t i = 0; i < items.size(); ++i) {
