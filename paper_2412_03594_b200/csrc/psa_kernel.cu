@@ -1275,6 +1275,8 @@ int launch_v2(const KParams& p_in, int32_t num_sms, void* stream) {
   const char* dbg_cta = std::getenv("PSA_DBG_CTA");
   p.dbg_cta = dbg_cta ? std::atoi(dbg_cta) : 0;
   if (dbg & 2) p.dec_slots = 2;
+  if (const char* tr = std::getenv("PSA_TILE_RING"))  // diagnostics: a shallower tile ring
+    p.tile_stages = std::max(2, std::min(p.tile_stages, std::atoi(tr)));
   if (dbg & 128) {  // one decode pipeline with the whole ring (diagnostics)
     p.dec_pipes = 1;
     while (p.dec_slots < dec::kMaxSlots && dec::pipe_stride(p.dec_slots + 1) <= budget) ++p.dec_slots;
