@@ -1,19 +1,32 @@
 #!/usr/bin/env python
 """Benchmark: fused prefix-shared attention on B200 (BASELINE.json metric).
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--config c2] [--impl ours|reference]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config c5] [--impl ours|reference]
 
-One step = one pass of the hot path over one synthetic token batch of the
-config (default c2 = BASELINE.json configs[1], Llama-3-8B-shaped decode: 16
-groups x 2k prefix x 32 requests x 256 distinct, 32/8 heads, d=128, bf16):
-ONE persistent kernel launch. Inputs (680 MB for c2) exceed the 126 MB L2, so
-no flush is needed between iterations.
+Workload (default ``c5`` = BASELINE.json configs[4], the config the metric's
+1/2/4/8-GPU numbers are quoted on: 1024 prefix groups x 4k-token prefix x 64
+requests x 256 distinct tokens, Llama-3-8B heads 32 q / 8 kv, d = 128, bf16;
+87 GB, fits one B200). One step = one pass of the hot path over the whole batch
+= ONE persistent kernel launch per rank (a CUDA graph replay of ``psa_run``).
+Inputs (87 GB) exceed the 126 MB L2 by far, so no flush is needed between steps.
+``--config c2/c3/c4/c1`` run the other BASELINE configs (secondary lines).
 
-Multi-GPU (torchrun, one process per GPU): groups are independent, so each
-rank processes its own batch of the config (weak scaling; per-group seeds
-offset by rank) with no data-path collective; the time is the max over ranks
-and ``value`` = that time / N, i.e. microseconds per config-batch for the
-whole job. c5 instead shards its 1024 groups across ranks by LPT (strong).
+Multi-GPU (torchrun, one process per GPU): groups are independent, so the
+batch's groups are LPT-partitioned across ranks (strong scaling: the total work
+is fixed); each rank generates only its own groups (per-group seeds, so the data
+is identical to the 1-GPU batch) and runs one launch; no data-path collective.
+``value`` = the max over ranks of the device time, in us per whole batch. The
+optional output gather (``gather``: per-slab NCCL all-gather overlapped with
+the next slab's launch) is reported beside the kernel-only number.
+
+After timing, a deterministic sample of (group, kv head) pairs of the TIMED
+output is checked against the float64 CPU oracle (``parity``).
+
+``--impl reference`` times the reference's own CPU implementation on the
+box's host cores: ``prefixbatch.attention.prefix_shared_attention`` imported
+from ``baseline/_ref`` (the unmodified reference, pip-installed there), or the
+float64 oracle port when that is absent. One step = one whole group (all kv
+heads) through it; ``value`` extrapolates to the batch (``extrapolation``).
 
 Prints ONE JSON line on rank 0.
 """
@@ -36,6 +49,8 @@ sys.path.insert(0, ROOT)
 
 METRIC = "prefix-shared attn µs/batch, TFLOP/s & HBM GB/s vs roofline at 1/2/4/8 GPU"
 FALLBACK_PEAKS = {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}
+PARITY_TOL = {"bf16": 2e-2, "f16": 2e-2, "f32": 1e-4, "f64": 1e-10}  # BASELINE.json north_star
+DEFAULT_CONFIG = "c5"
 
 
 def load_peaks():
@@ -46,6 +61,17 @@ def load_peaks():
         return pk, "measured (MEASURED_PEAKS.json)"
     except Exception:
         return dict(FALLBACK_PEAKS), "fallback (B200_PROFILING.md)"
+
+
+def cpu_model() -> str:
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
 
 
 class ClockSampler:
@@ -68,18 +94,21 @@ class ClockSampler:
         except Exception:
             self._nv = None
 
-    def _run(self):
+    def _sample(self):
         nv = self._nv
+        try:
+            self.samples.append(nv.nvmlDeviceGetClockInfo(self._h, nv.NVML_CLOCK_SM))
+            bits = nv.nvmlDeviceGetCurrentClocksEventReasons(self._h)
+            for b, name in self.REASONS.items():
+                if bits & b:
+                    self.reasons.add(name)
+        except Exception:
+            pass
+
+    def _run(self):
         while not self._stop.is_set():
-            try:
-                self.samples.append(nv.nvmlDeviceGetClockInfo(self._h, nv.NVML_CLOCK_SM))
-                bits = nv.nvmlDeviceGetCurrentClocksEventReasons(self._h)
-                for b, name in self.REASONS.items():
-                    if bits & b:
-                        self.reasons.add(name)
-            except Exception:
-                pass
-            time.sleep(0.005)
+            self._sample()
+            time.sleep(0.002)
 
     def __enter__(self):
         if self._nv is not None:
@@ -91,6 +120,8 @@ class ClockSampler:
         if self._thread is not None:
             self._stop.set()
             self._thread.join()
+            if not self.samples:
+                self._sample()
 
     def summary(self):
         return {"sm_mhz": statistics.median(self.samples) if self.samples else None,
@@ -98,17 +129,20 @@ class ClockSampler:
                 "samples": len(self.samples)}
 
 
-def dist_setup(args):
+def dist_setup():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+def dist_init(world, local):
     if world > 1:
         import torch.distributed as dist
         torch.cuda.set_device(local)
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     else:
         torch.cuda.set_device(0)
-    return world, rank, local
 
 
 def barrier(world):
@@ -126,58 +160,93 @@ def max_over_ranks(x: float, world: int) -> float:
     return float(t.item())
 
 
-def rank_spec(name: str, rank: int, world: int):
+def config_dict(spec, world: int) -> dict:
+    """The workload identity — printed identically by both arms."""
     from paper_2412_03594_b200 import workloads as W
-    spec = W.config(name)
+    off = W.offsets(spec)
+    cost = W.algorithmic_cost(spec)
+    return {"workload": spec.name, "groups": spec.G, "requests": int(len(off["cu_q"]) - 1),
+            "tokens": int(off["cu_q"][-1]), "prefix_keys": int(off["cu_prefix"][-1]),
+            "distinct_keys": int(off["cu_distinct"][-1]), "Hq": spec.Hq, "Hkv": spec.Hkv,
+            "head_dim": spec.d, "dtype": spec.dtype,
+            "parallelism": f"groups LPT-sharded over {world} GPUs" if world > 1 else "1 GPU",
+            "l2": f"inputs {cost['bytes'] / 1e6:.0f} MB vs 126 MB L2: no flush"}
+
+
+def rank_groups(spec, rank: int, world: int) -> list:
+    """This rank's groups: greedy LPT over the per-group cost model (psa_shard_groups)."""
     if world == 1:
-        return spec, "weak" if name != "c5" else "strong"
-    if name == "c5":
-        from paper_2412_03594_b200 import packed as P
-        off = W.offsets(spec)
-        cost = P.group_costs(off["cu_req"], off["cu_q"], off["cu_prefix"], off["cu_distinct"],
-                             spec.Hq, spec.Hkv, spec.d, spec.dv, spec.torch_dtype)
-        owner = P.shard_groups(cost, world)
-        return spec.subset([g for g in range(spec.G) if owner[g] == rank]), "strong"
-    # weak scaling: rank r processes its own copy of the config with distinct data
-    sub = spec.subset(range(spec.G))
-    sub.group_ids = [rank * spec.G + g for g in range(spec.G)]
-    return sub, "weak"
-
-
-def cpu_oracle_sample(spec, budget_s: float, max_pairs=None, seed=0):
-    """Time the CPU oracle (reference algorithm, float64 NumPy/OpenBLAS) on a
-    bounded sample of (group, kv head) calls of ``spec`` and extrapolate to the
-    whole batch. Inputs are generated on the host with the same per-group
-    seeds (CPU generator), so generation is excluded from the timing."""
-    from oracle import segmented as S
+        return list(range(spec.G))
+    from paper_2412_03594_b200 import packed as P
     from paper_2412_03594_b200 import workloads as W
-    rng = np.random.default_rng(seed)
-    pairs = [(g, h) for g in range(spec.G) for h in range(spec.Hkv)]
-    order = rng.permutation(len(pairs))
-    times, done = [], 0
-    t_start = time.perf_counter()
-    for i in order:
-        g, h = pairs[i]
-        sub = spec.subset([g])
-        b = W.make_batch(sub, "cpu")
-        host = {k: b[k].double().numpy() for k in ("q", "k_prefix", "v_prefix", "k_distinct",
-                                                     "v_distinct")}
-        t0 = time.perf_counter()
-        S.packed_group_head(host["q"], host["k_prefix"], host["v_prefix"], host["k_distinct"],
-                            host["v_distinct"], b["cu_req"], b["cu_q"], b["cu_prefix"],
-                            b["cu_distinct"], 0, h, spec.Hq, spec.Hkv)
-        times.append(time.perf_counter() - t0)
-        done += 1
-        if (max_pairs and done >= max_pairs) or time.perf_counter() - t_start > budget_s:
-            break
-    # weight each sampled pair by its group's share of work is unnecessary for uniform
-    # configs; for skewed configs scale by the per-group cost of the sample vs the total.
-    cost = np.array([W.algorithmic_cost(spec.subset([g]))["flops"] for g in range(spec.G)],
+    off = W.offsets(spec)
+    cost = P.group_costs(off["cu_req"], off["cu_q"], off["cu_prefix"], off["cu_distinct"],
+                         spec.Hq, spec.Hkv, spec.d, spec.dv, spec.torch_dtype)
+    owner = P.shard_groups(cost, world)
+    return [g for g in range(spec.G) if owner[g] == rank]
+
+
+# ---------------------------------------------------------------------------
+# The reference's CPU path (timed, never the GPU arm's compute)
+# ---------------------------------------------------------------------------
+
+def reference_impl():
+    """(prefix_shared_attention, SegmentedKV, kind, where): the unmodified reference from
+    baseline/_ref when it is installed there, else the float64 oracle port."""
+    ref = os.path.join(ROOT, "baseline", "_ref")
+    if os.path.isdir(os.path.join(ref, "prefixbatch")):
+        if ref not in sys.path:
+            sys.path.insert(0, ref)
+        try:
+            from prefixbatch.attention import SegmentedKV, prefix_shared_attention
+            return prefix_shared_attention, SegmentedKV, "reference", "baseline/_ref prefixbatch"
+        except Exception:
+            pass
+    from oracle import segmented as S
+
+    class _SKV:
+        def __init__(self, prefix, distinct):
+            self.prefix, self.distinct = prefix, distinct
+
+    def _psa(queries, kv, scale=None):
+        return S.group_attention(queries, kv.prefix, kv.distinct, scale)
+    return _psa, _SKV, "port", "oracle/segmented.py (float64 port)"
+
+
+def host_group(spec, g: int) -> dict:
+    """Group g of ``spec`` generated on the host (same per-group seeding scheme as the
+    device batch; the CPU generator's stream differs, the shapes are identical)."""
+    from paper_2412_03594_b200 import workloads as W
+    b = W.make_batch(spec.subset([g]), "cpu")
+    for k in ("q", "k_prefix", "v_prefix", "k_distinct", "v_distinct"):
+        b[k] = b[k].double().numpy()
+    return b
+
+
+def time_reference_group(psa, SKV, b, spec) -> float:
+    """Seconds for one whole group (every kv head) through the reference's entry point:
+    one prefix_shared_attention call per kv head, gqa heads stacked as rows
+    (attention.py:156-201; SURVEY.md §8(a) GQA adapter)."""
+    gqa = spec.Hq // spec.Hkv
+    cu_q, cu_d = b["cu_q"], b["cu_distinct"]
+    R = len(cu_q) - 1
+    calls = []
+    for h in range(spec.Hkv):
+        qs = [b["q"][cu_q[r]:cu_q[r + 1], h * gqa:(h + 1) * gqa].reshape(-1, spec.d) for r in range(R)]
+        pre = (b["k_prefix"][:, h], b["v_prefix"][:, h]) if b["k_prefix"].shape[0] else None
+        dis = [(b["k_distinct"][cu_d[r]:cu_d[r + 1], h], b["v_distinct"][cu_d[r]:cu_d[r + 1], h])
+               if cu_d[r + 1] > cu_d[r] else None for r in range(R)]
+        calls.append((qs, SKV(pre, dis)))
+    t0 = time.perf_counter()
+    for qs, kv in calls:
+        psa(qs, kv, 1.0 / np.sqrt(spec.d))
+    return time.perf_counter() - t0
+
+
+def group_weights(spec) -> np.ndarray:
+    from paper_2412_03594_b200 import workloads as W
+    return np.array([W.algorithmic_cost(spec.subset([g]))["flops"] for g in range(spec.G)],
                     dtype=np.float64)
-    sampled = [pairs[i][0] for i in order[:done]]
-    frac = cost[sampled].sum() / (cost.sum() * spec.Hkv)
-    total_s = sum(times) / frac
-    return total_s * 1e6, done, len(pairs)
 
 
 def blas_threads():
@@ -189,59 +258,194 @@ def blas_threads():
         return len(os.sched_getaffinity(0))
 
 
+def cpu_sample(spec, budget_s: float):
+    """CPU baseline beside the GPU arm: whole groups through the reference until the
+    budget is spent, extrapolated to the batch by FLOP share."""
+    psa, SKV, kind, where = reference_impl()
+    w = group_weights(spec)
+    order = np.random.default_rng(0).permutation(spec.G)
+    secs, done, t_start = 0.0, [], time.perf_counter()
+    for g in order:
+        secs += time_reference_group(psa, SKV, host_group(spec, int(g)), spec)
+        done.append(int(g))
+        if time.perf_counter() - t_start > budget_s:
+            break
+    frac = w[done].sum() / w.sum()
+    return secs / frac * 1e6, kind, where, len(done)
+
+
 def run_reference(args, world, rank):
-    """--impl reference: the reference's CPU algorithm (oracle port) on host cores."""
+    """--impl reference: the reference's CPU path on the host cores (rank 0 only)."""
     if rank != 0:
         return
     from paper_2412_03594_b200 import workloads as W
     spec = W.config(args.config)
-    per_step = []
+    psa, SKV, kind, where = reference_impl()
+    w = group_weights(spec)
+    per_step_s, groups = [], []
+    t_run0 = time.perf_counter()
     for step in range(args.warmup + args.steps):
-        us, done, total = cpu_oracle_sample(spec, budget_s=1e9, max_pairs=1, seed=step)
+        g = (step * 97) % spec.G   # deterministic group sample, one group per step
+        b = host_group(spec, g)
+        s = time_reference_group(psa, SKV, b, spec)
         if step >= args.warmup:
-            per_step.append(us)
-    value = statistics.mean(per_step)
+            per_step_s.append(s)
+            groups.append(g)
+    wall = time.perf_counter() - t_run0
+    frac = w[groups].sum() / w.sum()           # share of the batch's FLOP the steps covered
+    value_us = sum(per_step_s) / frac * 1e6    # whole batch, extrapolated
+    ms_step = statistics.mean(per_step_s) * 1e3
     cores = blas_threads()
-    line = {"metric": METRIC, "value": round(value, 1), "unit": "us/batch", "n_gpus": args.gpus,
-            "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(value / 1e3, 3),
-            "higher_is_better": False, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-            "data": "synthetic (per-group seeded N(0,1) / U(-10,10))", "impl": "reference",
-            "config": {"workload": args.config, "model": "llama-3-8b-shaped attention heads",
-                       "note": "each step = one (group, kv head) oracle call, extrapolated to the batch"},
-            "cpu_baseline": {"value": round(value, 1), "unit": "us/batch", "cores": cores,
-                             "kind": "port",
-                             "sample": f"1 of {spec.G * spec.Hkv} (group, kv-head) calls per step"},
-            "e2e": {"value": round(value, 1), "unit": "us/batch", "h2d_bytes_per_step": 0,
+    line = {"metric": METRIC, "value": round(value_us, 1), "unit": "us/batch", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_step, 3),
+            "higher_is_better": False, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (per-group seeded N(0,1) / U(-10,10), generated on the host, "
+                    "rounded to the config dtype, then float64)",
+            "impl": "reference", "config": config_dict(spec, world),
+            "extrapolation": {"unit_per_step": "one whole group (all kv heads)",
+                              "groups_timed": len(groups), "groups_total": spec.G,
+                              "flop_share_timed": round(float(frac), 6),
+                              "value_is": "sum of timed step seconds / flop_share_timed"},
+            "wall_s": round(wall, 2),
+            "cpu_baseline": {"value": round(value_us, 1), "unit": "us/batch", "cores": cores,
+                             "kind": kind, "impl": where, "cpu_model": cpu_model(),
+                             "sample": f"{len(groups)} of {spec.G} groups, one per step "
+                                       "(every kv head, one prefix_shared_attention call each)"},
+            "e2e": {"value": round(value_us, 1), "unit": "us/batch", "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------------------
+# GPU arm helpers
+# ---------------------------------------------------------------------------
+
+def graph_kernel_nodes(graph) -> list:
+    """Kernel nodes of a captured CUDA graph (names when the runtime reports them)."""
+    try:
+        from cuda.bindings import runtime as rt
+        g = graph.raw_cuda_graph()
+        err, _, n = rt.cudaGraphGetNodes(g, 0)
+        err, nodes, n = rt.cudaGraphGetNodes(g, n)
+        names = []
+        for nd in nodes:
+            err, ty = rt.cudaGraphNodeGetType(nd)
+            if ty == rt.cudaGraphNodeType.cudaGraphNodeTypeKernel:
+                name = "kernel"
+                try:
+                    err, prm = rt.cudaGraphKernelNodeGetParams(nd)
+                    err, nm = rt.cudaFuncGetName(prm.func)
+                    if err == rt.cudaError_t.cudaSuccess and nm:
+                        name = nm.decode() if isinstance(nm, bytes) else str(nm)
+                except Exception:
+                    pass
+                names.append(name)
+        return names
+    except Exception as e:  # pragma: no cover - diagnostics only
+        return [f"unknown ({type(e).__name__})"]
+
+
+def parity_check(spec, b, out, n_pairs: int = 8) -> dict:
+    """Deterministic sample of (group, kv head) pairs of the timed output vs the oracle."""
+    from oracle import segmented as S
+    G = spec.G
+    gs = sorted({int(x) for x in np.linspace(0, G - 1, min(n_pairs, G))})
+    worst, pairs = 0.0, []
+    cu_req, cu_q, cu_p, cu_d = b["cu_req"], b["cu_q"], b["cu_prefix"], b["cu_distinct"]
+    gqa = spec.Hq // spec.Hkv
+    for i, g in enumerate(gs):
+        h = (i * 3) % spec.Hkv
+        r0, r1 = int(cu_req[g]), int(cu_req[g + 1])
+        t0, t1 = int(cu_q[r0]), int(cu_q[r1])
+        p0, p1 = int(cu_p[g]), int(cu_p[g + 1])
+        d0, d1 = int(cu_d[r0]), int(cu_d[r1])
+        host = lambda t, a, z: t[a:z].double().cpu().numpy()  # noqa: E731
+        res = S.packed_group_head(host(b["q"], t0, t1), host(b["k_prefix"], p0, p1),
+                                  host(b["v_prefix"], p0, p1), host(b["k_distinct"], d0, d1),
+                                  host(b["v_distinct"], d0, d1), np.array([0, r1 - r0]),
+                                  cu_q[r0:r1 + 1] - t0, np.array([0, p1 - p0]),
+                                  cu_d[r0:r1 + 1] - d0, 0, h, spec.Hq, spec.Hkv)
+        got = out[t0:t1, h * gqa:(h + 1) * gqa].double().cpu().numpy()
+        want = np.concatenate([r.reshape(-1, gqa, spec.dv) for r in res])
+        err = float(np.abs(got - want).max())
+        if spec.dtype == "f32":
+            err /= max(float(np.abs(want).max()), 1e-30)
+        worst = max(worst, err)
+        pairs.append([g, h])
+    tol = PARITY_TOL[spec.dtype]
+    return {"max_abs_err" if spec.dtype != "f32" else "normwise_err": worst, "tol": tol,
+            "ok": bool(worst <= tol), "pairs": pairs, "checker": "oracle/segmented.py float64"}
+
+
+def time_e2e(spec, b, dev, opts, world, steps: int):
+    """End to end through the public host-buffer API (HostStreamedAttention): every step
+    copies the whole batch's inputs from pinned host memory to the device and the output
+    back, group slab by group slab, overlapped with the per-slab launches."""
+    from paper_2412_03594_b200 import streamed as ST
+    keys = ("q", "k_prefix", "v_prefix", "k_distinct", "v_distinct")
+    host = {}
+    for k in keys:
+        h = torch.empty(b[k].shape, dtype=b[k].dtype, pin_memory=True)
+        h.copy_(b[k])
+        host[k] = h
+    out_host = torch.empty((b["q"].shape[0], spec.Hq, spec.dv), dtype=spec.torch_dtype,
+                           pin_memory=True)
+    run = ST.HostStreamedAttention(b["cu_req"], b["cu_q"], b["cu_prefix"], b["cu_distinct"],
+                                   spec.Hq, spec.Hkv, spec.d, spec.dv, spec.torch_dtype, dev,
+                                   options=opts)
+    args = [host[k] for k in keys]
+    run(*args, out_host)
+    torch.cuda.synchronize()
+    barrier(world)
+    stream = torch.cuda.current_stream(dev)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(steps):
+        run(*args, out_host)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    ms = max_over_ranks(e0.elapsed_time(e1) / steps, world)
+    h2d, d2h = run.bytes_per_call()
+    del host, args
+    return {"value": round(ms * 1e3, 1), "unit": "us/batch", "h2d_bytes_per_step": int(h2d),
+            "d2h_bytes_per_step": int(d2h), "steps": steps, "slabs": len(run.slabs),
+            "gpu_launches_per_step": run.launches_per_call,
+            "api": "paper_2412_03594_b200.streamed.HostStreamedAttention (pinned host in/out)",
+            "h2d_gbs": round(h2d / (ms * 1e-3) / 1e9, 1)}
 
 
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=200)
-    ap.add_argument("--warmup", type=int, default=10)
-    ap.add_argument("--config", default="c2")
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--config", default=DEFAULT_CONFIG)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--cpu-budget", type=float, default=12.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--e2e-steps", type=int, default=0, help="0 = min(steps, 3)")
+    ap.add_argument("--no-parity", action="store_true")
+    ap.add_argument("--no-gather", action="store_true")
     ap.add_argument("--disable-tiles", action="store_true")
     ap.add_argument("--no-graph", action="store_true",
                     help="launch through psa_run every step instead of replaying a CUDA graph")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
 
-    world, rank, local = dist_setup(args)
+    world, rank, local = dist_setup()
     if args.impl == "reference":
         run_reference(args, world, rank)
         return
+    dist_init(world, local)
 
     from paper_2412_03594_b200 import packed as P
     from paper_2412_03594_b200 import workloads as W
 
     dev = torch.device("cuda", local)
-    spec, scaling = rank_spec(args.config, rank, world)
+    full = W.config(args.config)
+    groups = rank_groups(full, rank, world)
+    spec = full.subset(groups)
     b = W.make_batch(spec, dev)
     opts = P.PlanOptions(disable_tiles=int(args.disable_tiles))
     op = P.PrefixSharedAttention(b["cu_req"], b["cu_q"], b["cu_prefix"], b["cu_distinct"],
@@ -249,29 +453,35 @@ def main():
                                  options=opts)
     inputs = (b["q"], b["k_prefix"], b["v_prefix"], b["k_distinct"], b["v_distinct"])
     out = torch.empty((b["q"].shape[0], spec.Hq, spec.dv), dtype=spec.torch_dtype, device=dev)
+    out.fill_(float("nan"))  # parity sees only what the timed launches wrote
     stream = torch.cuda.current_stream(dev)
 
-    # The timed step is one launch of the planned op. By default it is captured once
-    # into a CUDA graph (what an engine does per layer) so host-side launch cost
-    # (tensor-map encoding, ctypes) is off the device timeline; --no-graph launches
-    # through psa_run every step.
+    # The timed step is one launch of the planned op, captured once into a CUDA graph
+    # (what an engine does per layer) so host-side launch cost stays off the device
+    # timeline; --no-graph launches through psa_run every step.
     step = lambda: op(*inputs, out=out)  # noqa: E731
     for _ in range(args.warmup):
         step()
     torch.cuda.synchronize()
+    kernels_per_step = 1
+    kernel_names = ["psa_run (direct launch)"]
     if not args.no_graph:
         side = torch.cuda.Stream(dev)
         side.wait_stream(stream)
-        graph = torch.cuda.CUDAGraph()
+        graph = torch.cuda.CUDAGraph(keep_graph=True)
         with torch.cuda.graph(graph, stream=side):
             op(*inputs, out=out, stream=side)
+        graph.instantiate()
         torch.cuda.synchronize()
+        kernel_names = graph_kernel_nodes(graph)
+        kernels_per_step = len(kernel_names)
         step = graph.replay
         for _ in range(args.warmup):
             step()
         torch.cuda.synchronize()
-    # correctness guard on the bench batch itself (one sampled group, oracle on host)
-    sampler = ClockSampler(torch.cuda.current_device() if world == 1 else local)
+    out.fill_(float("nan"))
+    torch.cuda.synchronize()
+    sampler = ClockSampler(local)
     start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     barrier(world)
     torch.cuda.synchronize()
@@ -286,96 +496,91 @@ def main():
     ms = max_over_ranks(ms_rank, world)
     err_bits = op.device_error()
 
-    # ---- end to end through the public packed API with host buffers ------------
+    parity = None
+    if not args.no_parity:
+        parity = parity_check(spec, b, out)
+
+    gather = None
+    if world > 1 and not args.no_gather:
+        from paper_2412_03594_b200 import distributed as D
+        gather = D.time_slab_gather(spec, b, dev, opts, world, steps=max(3, min(args.steps, 10)),
+                                    barrier=lambda: barrier(world),
+                                    max_over_ranks=lambda x: max_over_ranks(x, world))
+
     e2e = None
     if not args.no_e2e:
-        host = [t.cpu().pin_memory() for t in inputs]
-        h2d = sum(t.numel() * t.element_size() for t in host)
-        out_host = torch.empty(out.shape, dtype=out.dtype).pin_memory()
-        d2h = out_host.numel() * out_host.element_size()
-        dev_in = [torch.empty_like(t, device=dev) for t in host]
-        e_steps = max(3, min(args.steps, 20))
+        e_steps = args.e2e_steps or min(args.steps, 3)
+        e2e = time_e2e(spec, b, dev, opts, world, e_steps)
 
-        def e2e_step():
-            for dst, src in zip(dev_in, host):
-                dst.copy_(src, non_blocking=True)
-            o = P.prefix_shared_attention_packed(*dev_in, b["cu_req"], b["cu_q"], b["cu_prefix"],
-                                                 b["cu_distinct"], spec.Hkv, options=opts)
-            out_host.copy_(o, non_blocking=True)
-
-        for _ in range(2):
-            e2e_step()
-        torch.cuda.synchronize()
-        barrier(world)
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record(stream)
-        for _ in range(e_steps):
-            e2e_step()
-        e1.record(stream)
-        torch.cuda.synchronize()
-        e_ms = max_over_ranks(e0.elapsed_time(e1) / e_steps, world)
-        e2e = {"value": round(e_ms * 1e3 / world, 1), "unit": "us/batch",
-               "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h), "steps": e_steps}
-
-    cost = W.algorithmic_cost(spec)
+    cost_rank = W.algorithmic_cost(spec)
+    cost = W.algorithmic_cost(full)
     peaks, peaks_src = load_peaks()
-    us_per_batch = ms * 1e3 / world
-    achieved_gbs = cost["bytes"] / (ms_rank * 1e-3) / 1e9
-    achieved_tflops = cost["flops"] / (ms_rank * 1e-3) / 1e12
+    achieved_gbs = cost_rank["bytes"] / (ms_rank * 1e-3) / 1e9
+    achieved_tflops = cost_rank["flops"] / (ms_rank * 1e-3) / 1e12
     hbm_peak = float(peaks["hbm_gbs"])
     tc_peak = float(peaks["bf16_tflops"])
-    t_roof = max(cost["bytes"] / (hbm_peak * 1e9), cost["flops"] / (tc_peak * 1e12))
-    bound = "hbm" if cost["bytes"] / (hbm_peak * 1e9) >= cost["flops"] / (tc_peak * 1e12) else "tensor"
+    t_hbm = cost_rank["bytes"] / (hbm_peak * 1e9)
+    t_tc = cost_rank["flops"] / (tc_peak * 1e12)
+    bound = "hbm" if t_hbm >= t_tc else "tensor"
     achieved, peak, unit = ((achieved_gbs, hbm_peak, "GB/s") if bound == "hbm"
                             else (achieved_tflops, tc_peak, "TFLOP/s"))
     traffic = None
     tpath = os.path.join(ROOT, "profiles", "traffic.json")
-    if os.path.exists(tpath):
+    if os.path.exists(tpath) and world == 1:
         with open(tpath) as f:
             traffic = json.load(f).get(args.config)
 
     line = {
-        "metric": METRIC, "value": round(us_per_batch, 2), "unit": "us/batch", "n_gpus": world,
+        "metric": METRIC, "value": round(ms * 1e3, 2), "unit": "us/batch", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 4),
-        "higher_is_better": False, "scaling": scaling, "vs_baseline": None,
-        "dtype": {"bf16": "bf16", "f16": "f16", "f32": "f32", "f64": "f64"}[spec.dtype],
+        "higher_is_better": False, "scaling": "strong", "vs_baseline": None,
+        "dtype": spec.dtype,
         "data": "synthetic (per-group seeded N(0,1) / U(-10,10), generated on device)",
-        "config": {"workload": args.config, "groups_per_rank": spec.G, "Hq": spec.Hq,
-                   "Hkv": spec.Hkv, "head_dim": spec.d,
-                   "tokens_per_rank": int(b["cu_q"][-1]),
-                   "parallelism": f"group-sharded x{world}" if world > 1 else "1 GPU",
-                   "launch": "psa_run" if args.no_graph else "CUDA graph replay of one psa_run",
-                   "l2": f"inputs {cost['bytes'] / 1e6:.0f} MB > 126 MB L2, no flush",
-                   "plan_items": op.num_items},
-        "tflops": round(achieved_tflops * world, 2), "hbm_gbs": round(achieved_gbs * world, 1),
-        "t_roof_us": round(t_roof * 1e6, 2),
+        "config": config_dict(full, world),
+        "run": {"groups_this_rank": spec.G, "tokens_this_rank": int(b["cu_q"][-1]),
+                "launch": "psa_run" if args.no_graph else "CUDA graph replay of one psa_run",
+                "plan_items": op.num_items},
+        "tflops": round(cost["flops"] / (ms * 1e-3) / 1e12, 2),
+        "hbm_gbs": round(cost["bytes"] / (ms * 1e-3) / 1e9, 1),
+        "t_roof_us": round(max(t_hbm, t_tc) * 1e6, 2),
         # BASELINE.json's literal split: the slower of the prefix FLOP at tensor peak and
         # the distinct KV bytes at HBM bandwidth (ignores prefix KV, Q and O traffic)
-        "t_roof_split_us": round(max(cost["flops_prefix"] / (tc_peak * 1e12),
-                                     cost["bytes_distinct"] / (hbm_peak * 1e9)) * 1e6, 2),
-        "frac_split": round(max(cost["flops_prefix"] / (tc_peak * 1e12),
-                                cost["bytes_distinct"] / (hbm_peak * 1e9)) / (ms_rank * 1e-3), 4),
+        "t_roof_split_us": round(max(cost_rank["flops_prefix"] / (tc_peak * 1e12),
+                                     cost_rank["bytes_distinct"] / (hbm_peak * 1e9)) * 1e6, 2),
         "roofline": {"bound": bound, "achieved": round(achieved, 2), "peak": peak, "unit": unit,
                      "frac": round(achieved / peak, 4), "traffic": traffic,
-                     "peak_source": peaks_src, "t_roof_over_t": round(t_roof / (ms_rank * 1e-3), 4),
-                     "algorithmic_bytes": cost["bytes"], "algorithmic_flops": cost["flops"]},
-        "gpu_launches": args.steps,
+                     "kernel": "psa_v2 (the only kernel in the timed region)",
+                     "peak_source": peaks_src,
+                     "algorithmic_bytes_per_launch": cost_rank["bytes"],
+                     "algorithmic_flops_per_launch": cost_rank["flops"],
+                     "launch_us": round(ms_rank * 1e3, 2)},
+        "gpu_launches": kernels_per_step * args.steps,
+        "gpu_kernels_per_step": kernel_names,
         "device_error_bits": err_bits,
         "clocks": sampler.summary(),
     }
+    if parity is not None:
+        line["parity"] = parity
+    if gather is not None:
+        line["gather"] = gather
     if e2e is not None:
         line["e2e"] = e2e
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        us_cpu, done, total = cpu_oracle_sample(spec, budget_s=args.cpu_budget)
+        us_cpu, kind, where, n = cpu_sample(spec, args.cpu_budget)
         line["cpu_baseline"] = {"value": round(us_cpu, 1), "unit": "us/batch",
-                                "cores": blas_threads(), "kind": "port",
-                                "sample": f"{done} of {total} (group, kv-head) oracle calls, "
+                                "cores": blas_threads(), "kind": kind, "impl": where,
+                                "cpu_model": cpu_model(),
+                                "sample": f"{n} of {spec.G} whole groups (every kv head), "
                                           "extrapolated by FLOP share"}
     if rank == 0:
         print(json.dumps(line), flush=True)
+    if parity is not None and not parity["ok"]:
+        sys.stderr.write(f"PARITY FAILED: {parity}\n")
     if world > 1:
         import torch.distributed as dist
         dist.destroy_process_group()
+    if parity is not None and not parity["ok"]:
+        sys.exit(1)
 
 
 if __name__ == "__main__":

@@ -200,7 +200,7 @@ psa_status psa_count_nonfinite(const void* data, int64_t n, int32_t dtype, int32
 psa_status psa_debug_set_trace(void* buf, int64_t capacity_items);
 
 /* Group -> rank partition for multi-GPU sharding: greedy LPT
- * over per-group costs, deterministic ties (bit-exact with oracle/shard.py). */
+ * over per-group costs, deterministic ties (bit-exact with oracle/plan.py shard_groups). */
 psa_status psa_shard_groups(int32_t num_groups, const int64_t* group_cost, int32_t world_size,
                             int32_t* owner);
 /* Per-group cost used by psa_shard_groups (same model as the planner). */

@@ -13,9 +13,9 @@ Contents
                it once per (group, kv-head).
 ``plan``       pure-Python restatement of the work-item planner implemented in
                C++ inside ``libpsa.so`` (``psa_plan``); the int32 tables the two
-               produce must be byte-identical.
-``shard``      pure-Python restatement of the group→rank LPT partition
-               (``psa_shard_groups``).
+               produce must be byte-identical. ``plan.group_costs`` /
+               ``plan.shard_groups`` restate the group→rank LPT partition
+               (``psa_group_costs`` / ``psa_shard_groups``).
 
 Parity pinning: ``segmented`` is checked against golden vectors produced by
 importing the reference itself (``tests/golden/make_golden.py``, run in the

@@ -18,7 +18,7 @@ PSA_OK, PSA_INVALID_ARGUMENT, PSA_UNSUPPORTED, PSA_CUDA_ERROR = 0, 1, 2, 3
 DTYPE_F32, DTYPE_BF16, DTYPE_F16, DTYPE_F64 = 0, 1, 2, 3
 FLAG_PARTIAL_OUT = 1
 FLAG_CAUSAL = 2  # include/psa.h PSA_FLAG_CAUSAL (extension: causal prefill chunks)
-ABI_VERSION = 2  # include/psa.h PSA_ABI_VERSION
+ABI_VERSION = 3  # include/psa.h PSA_ABI_VERSION (checked at load)
 
 
 class Problem(C.Structure):
@@ -95,6 +95,18 @@ class NativeError(RuntimeError):
         self.status = status
 
 
+def _bind(handle):
+    for name, res, args in SIGNATURES:
+        fn = getattr(handle, name)
+        fn.restype = res
+        fn.argtypes = args
+    got = handle.psa_abi_version()
+    if got != ABI_VERSION:
+        raise RuntimeError(f"libpsa.so ABI version {got}, this binding expects {ABI_VERSION}: "
+                           "rebuild with `python -m paper_2412_03594_b200.build`")
+    return handle
+
+
 def lib():
     """Load libpsa.so (building it first when the sources are newer and nvcc exists)."""
     global _lib
@@ -105,12 +117,7 @@ def lib():
             return _lib
         alt = os.environ.get("PSA_LIB_PATH")  # diagnostics: A/B another build of the library
         if alt:
-            handle = C.CDLL(alt)
-            for name, res, args in SIGNATURES:
-                fn = getattr(handle, name)
-                fn.restype = res
-                fn.argtypes = args
-            _lib = handle
+            _lib = _bind(C.CDLL(alt))
             return _lib
         if os.environ.get("PSA_NO_BUILD") != "1":
             try:
@@ -122,12 +129,7 @@ def lib():
         if not os.path.exists(LIB_PATH):
             raise RuntimeError(f"libpsa.so not found at {LIB_PATH}; run "
                                "`python -m paper_2412_03594_b200.build` (no CPU fallback exists)")
-        handle = C.CDLL(LIB_PATH)
-        for name, res, args in SIGNATURES:
-            fn = getattr(handle, name)
-            fn.restype = res
-            fn.argtypes = args
-        _lib = handle
+        _lib = _bind(C.CDLL(LIB_PATH))
     return _lib
 
 

@@ -74,6 +74,11 @@ def prepare(state, batch) -> KernelBatch:
     ``step``."""
     bs = int(state.config.block_size)
     alloc = state.allocator
+    policy = getattr(state.config, "policy", "batchllm")
+    if policy != "batchllm":
+        # fcfs-cap(-lru) states skip cache-hit prompt tokens (reused_tokens) whose KV
+        # lives in another owner's blocks: D below would silently leave them out.
+        raise ValueError(f"prepare() maps batchllm scheduler states only (got {policy!r})")
     # 1. post-step lengths + the grows step() will perform, in entry order
     groups = {}   # key -> dict(owner, P, reqs=[])
     order = []
@@ -90,6 +95,9 @@ def prepare(state, batch) -> KernelBatch:
             order.append(key)
             continue
         r = state.requests[e.owner]
+        if getattr(r, "reused_tokens", 0):
+            raise ValueError(f"request {r.id} has {r.reused_tokens} reused (cache-hit) tokens; "
+                             "their KV is not in its own blocks")
         if e.kind == DISTINCT_CHUNK:
             D = r.suffix_done + e.tokens
         elif e.kind == DECODE:
@@ -114,13 +122,21 @@ def prepare(state, batch) -> KernelBatch:
         grp = groups[key]
         P = grp["P"]
         if P:
-            ppages.extend(alloc.blocks_of(grp["owner"])[:_blocks_for(P, bs)])
+            blocks = alloc.blocks_of(grp["owner"])
+            need = _blocks_for(P, bs)
+            if len(blocks) < need:  # a short list would shift every later page-table base
+                raise ValueError(f"{grp['owner']} holds {len(blocks)} blocks, {need} needed")
+            ppages.extend(blocks[:need])
         cu_prefix.append(cu_prefix[-1] + P)
         for ei, n, rid, D in grp["reqs"]:
             cu_q.append(cu_q[-1] + n)
             cu_distinct.append(cu_distinct[-1] + D)
             if D:
-                dpages.extend(alloc.blocks_of(rid)[:_blocks_for(D, bs)])
+                blocks = alloc.blocks_of(rid)
+                need = _blocks_for(D, bs)
+                if len(blocks) < need:
+                    raise ValueError(f"request {rid} holds {len(blocks)} blocks, {need} needed")
+                dpages.extend(blocks[:need])
             tok_e.extend([ei] * n)
             tok_o.extend(range(n))
             req_e.append(ei)

@@ -25,6 +25,7 @@ struct psa_plan {
   bool use_v2 = false;
   std::vector<int64_t> group_tok0, group_pbase, req_dbase;
   std::vector<int32_t> tok_lim;  // causal key limits per token (PSA_FLAG_CAUSAL)
+  bool causal_ok = true;         // every request satisfies n_q <= D (D > 0) or n_q <= P
   int32_t page_size = 0;
   int64_t prefix_pages = 0, distinct_pages = 0;  // paged: page-table lengths
   int64_t num_tokens = 0, prefix_keys = 0, distinct_keys = 0;
@@ -199,11 +200,14 @@ psa_status psa_plan_create(const psa_problem* prob, const psa_plan_opts* opts, p
   pl->distinct_pages = pages;
   // causal limits (include/psa.h PSA_FLAG_CAUSAL): last visible prefix / distinct key
   pl->tok_lim.resize(size_t(in.cu_q[in.R]) * 2);
+  pl->causal_ok = true;
   for (int32_t g = 0; g < in.G; ++g) {
     const int64_t P = in.cu_prefix[g + 1] - in.cu_prefix[g];
     for (int64_t r = in.cu_req[g]; r < in.cu_req[g + 1]; ++r) {
       const int64_t nq = in.cu_q[r + 1] - in.cu_q[r];
       const int64_t D = in.cu_distinct[r + 1] - in.cu_distinct[r];
+      // the limits below can only express chunks that end the keys they attend to
+      if (nq > (D > 0 ? D : P)) pl->causal_ok = false;
       for (int64_t j = 0; j < nq; ++j) {
         const int64_t t = in.cu_q[r] + j;
         const int64_t lp = D > 0 ? P - 1 : P - nq + j;
@@ -319,6 +323,10 @@ psa_status psa_run(const psa_problem* prob, const psa_plan* pl, void* ws, size_t
   if ((prob->flags & PSA_FLAG_CAUSAL) && !pl->use_v2)
     return fail(PSA_UNSUPPORTED,
                 "causal masking needs the v2 kernel (bf16/f16, head_dim == value_dim == 128)");
+  if ((prob->flags & PSA_FLAG_CAUSAL) && !pl->causal_ok)
+    return fail(PSA_INVALID_ARGUMENT,
+                "causal masking needs n_q <= D (requests with distinct KV) or n_q <= P "
+                "(prefix-only chunks): the query tokens must be the last keys they attend to");
   k.ws_o = base + pl->off_wso;
   k.ws_ml = base + pl->off_wsml;
   k.unit_cnt = reinterpret_cast<int32_t*>(base + pl->off_cnt);
@@ -335,7 +343,11 @@ psa_status psa_run(const psa_problem* prob, const psa_plan* pl, void* ws, size_t
   }
   k.Hq = in.Hq; k.Hkv = in.Hkv; k.gqa = in.Hq / in.Hkv; k.d = in.d; k.dv = in.dv;
   k.flags = prob->flags;
-  k.scale = prob->scale;
+  // scale == 0 (uniform weights; allowed by naive_attention, attention.py:135-136): the
+  // softmaxes mask a key by setting its raw score to -inf before scaling, and -inf * 0
+  // is NaN. A scale of 1e-30 gives every finite logit |s| * 1e-30 < 2^-60 — exp of it
+  // is exactly 1 in fp32 and fp64 — while masked keys stay at -inf.
+  k.scale = prob->scale > 0 ? prob->scale : 1e-30;
   k.trace = g_trace;
   k.trace_cap = int32_t(g_trace_cap);
   k.use_tiles = pl->use_tiles ? 1 : 0;

@@ -192,6 +192,17 @@ class PrefixSharedAttention:
             raise ValidationError(f"{name} must be a contiguous [{rows}, {heads}, {dim}] tensor, "
                                   f"got {tuple(t.shape)}")
 
+    def _check_out(self, name, t, shape: tuple, dtype: torch.dtype):
+        """Caller-supplied output buffers: psa_run cannot check sizes, so a wrong shape,
+        dtype, layout or device here would be an out-of-bounds device write."""
+        if not isinstance(t, torch.Tensor):
+            raise ValidationError(f"{name} must be a torch tensor")
+        if t.device != self.device or t.dtype != dtype or tuple(t.shape) != shape \
+                or not t.is_contiguous():
+            raise ValidationError(f"{name} must be a contiguous {dtype} tensor of shape "
+                                  f"{list(shape)} on {self.device}, got {t.dtype} "
+                                  f"{list(t.shape)} on {t.device}")
+
     def _check_pages(self, name, t, n):
         if n == 0:
             return
@@ -235,11 +246,22 @@ class PrefixSharedAttention:
             self._check("v_distinct", v_distinct, self.num_distinct_keys, self.Hkv, self.dv)
         flags = 0
         m_out = l_out = None
+        acc = acc_dtype(self.dtype)
         if partial is not None:
             flags = L.FLAG_PARTIAL_OUT
+            if not isinstance(partial, (tuple, list)) or len(partial) != 3:
+                raise ValidationError("partial must be a tuple (o, m, l)")
             out, m_out, l_out = partial
+            # the kernel writes unnormalised rows in the accumulate type
+            self._check_out("partial o", out, (T, self.Hq, self.dv), acc)
+            self._check_out("partial m", m_out, (T, self.Hq), acc)
+            self._check_out("partial l", l_out, (T, self.Hq), acc)
         elif out is None:
             out = torch.empty((T, self.Hq, self.dv), dtype=self.dtype, device=self.device)
+        else:
+            self._check_out("out", out, (T, self.Hq, self.dv), self.dtype)
+        if lse is not None:
+            self._check_out("lse", lse, (T, self.Hq), torch.float32)
         if causal:
             flags |= L.FLAG_CAUSAL
         prob = self._problem(flags)

@@ -33,7 +33,7 @@ def test_library_exports_every_declared_symbol():
 
 def test_abi_version_and_error_channel():
     lib = L.lib()
-    assert lib.psa_abi_version() == 3  # psa_problem paged-KV fields
+    assert lib.psa_abi_version() == 3 == L.ABI_VERSION  # checked by _lib.lib() at load
     # a NULL problem is rejected with INVALID_ARGUMENT and a message, no CUDA needed
     h = ctypes.c_void_p()
     st = lib.psa_plan_create(None, None, ctypes.byref(h))

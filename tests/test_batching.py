@@ -84,3 +84,30 @@ def test_fixture_reproduces_from_the_reference_scheduler():
     for i, (_batch, kb, _state) in enumerate(records):
         for k in M.KEYS:
             assert np.array_equal(getattr(kb, k), FIX[f"b{i}_{k}"]), (i, k)
+
+
+def test_prepare_rejects_non_batchllm_states_and_short_block_lists():
+    """prepare() guards: fcfs_cap states and cache-hit tokens are not
+    expressible; a block list shorter than the segment would shift page bases."""
+    from types import SimpleNamespace as NS
+    cfg = NS(block_size=16, policy="fcfs_cap")
+    st = NS(config=cfg, allocator=None, groups=[], requests={})
+    with pytest.raises(ValueError, match="batchllm"):
+        B.prepare(st, NS(entries=[]))
+
+    class Alloc:
+        def grow(self, owner, n):
+            pass
+
+        def blocks_of(self, owner):
+            return [0]  # one block, fewer than the 3 a 40-token segment needs
+
+    req = NS(id="r0", group=None, suffix_done=0, decode_done=0, reused_tokens=0)
+    st = NS(config=NS(block_size=16, policy="batchllm"), allocator=Alloc(), groups=[],
+            requests={"r0": req})
+    entry = NS(kind=B.DISTINCT_CHUNK, owner="r0", tokens=40)
+    with pytest.raises(ValueError, match="blocks"):
+        B.prepare(st, NS(entries=[entry]))
+    req.reused_tokens = 16
+    with pytest.raises(ValueError, match="reused"):
+        B.prepare(st, NS(entries=[entry]))

@@ -60,3 +60,36 @@ def test_causal_needs_the_v2_kernel():
     spec = W.Spec("c64", 4, 4, 64, 64, "bf16", "normal", [64], [[(8, 8)]], seed=1)
     with pytest.raises(ValidationError, match="causal"):
         _run(spec, True)
+
+
+@pytest.mark.parametrize("reqs,P", [([(40, 20)], 64), ([(80, 0)], 64)],
+                         ids=["nq_gt_D", "prefix_only_nq_gt_P"])
+def test_causal_rejects_chunks_longer_than_their_keys(reqs, P):
+    """n_q > D (or n_q > P without distinct KV) cannot be expressed by the per-token key
+    limits: it would leak later prefix keys to the first tokens — rejected."""
+    spec = W.Spec("bad_causal", 8, 2, 128, 128, "bf16", "normal", [P], [reqs], seed=3)
+    with pytest.raises(ValidationError, match="n_q <= D"):
+        _run(spec, True)
+
+
+def test_zero_scale_is_a_uniform_average_on_tiles():
+    """scale == 0 (naive_attention allows it): every key weighs the same, also on the
+    tile path with a partial last key block (the mask must not produce NaN)."""
+    spec = W.Spec("scale0", 16, 4, 128, 128, "bf16", "normal", [200],
+                  [[(1, 37)] * 40], seed=5)
+    b = W.make_batch(spec, "cuda")
+    op = P.PrefixSharedAttention(b["cu_req"], b["cu_q"], b["cu_prefix"], b["cu_distinct"],
+                                 spec.Hq, spec.Hkv, spec.d, spec.dv, spec.torch_dtype, "cuda",
+                                 scale=0.0)
+    out = op(b["q"], b["k_prefix"], b["v_prefix"], b["k_distinct"], b["v_distinct"])
+    torch.cuda.synchronize()
+    assert not torch.isnan(out).any()
+    kp, vp = b["k_prefix"].double(), b["v_prefix"].double()
+    vd = b["v_distinct"].double()
+    gqa = spec.Hq // spec.Hkv
+    for r in (0, 17, 39):
+        for h in range(spec.Hkv):
+            keys = torch.cat([vp[:, h], vd[r * 37:(r + 1) * 37, h]])
+            want = keys.mean(0)
+            got = out[r, h * gqa:(h + 1) * gqa].double()
+            assert float((got - want).abs().max()) <= 2e-2

@@ -148,16 +148,46 @@ def test_lse_output_matches_oracle():
                     assert abs(lse[tok, hq].item() - ref) < 2e-3
 
 
-@pytest.mark.parametrize("name", ["c1", "c2", "c3", "c4"])
+@pytest.mark.parametrize("name", ["c1", "c2", "c3", "c4", "c5"])
 def test_bench_config_parity_against_oracle(name):
-    """Full-size bench batches; the oracle checks a sample of (group, kv head) pairs."""
+    """Full-size bench batches (c5: all 1024 groups, 87 GB, one launch); the oracle
+    checks a sample of (group, kv head) pairs and every row must be written."""
     spec = W.config(name)
     b = W.make_batch(spec, "cuda")
     op = P.PrefixSharedAttention(b["cu_req"], b["cu_q"], b["cu_prefix"], b["cu_distinct"],
                                  spec.Hq, spec.Hkv, spec.d, spec.dv, spec.torch_dtype, "cuda")
-    out = op(b["q"], b["k_prefix"], b["v_prefix"], b["k_distinct"], b["v_distinct"])
+    out = torch.full((b["q"].shape[0], spec.Hq, spec.dv), float("nan"), dtype=spec.torch_dtype,
+                     device="cuda")
+    op(b["q"], b["k_prefix"], b["v_prefix"], b["k_distinct"], b["v_distinct"], out=out)
     torch.cuda.synchronize()
-    check_sampled_groups(spec, b, out, n_groups=3, n_heads=2)
+    assert op.device_error() == 0
+    assert not torch.isnan(out).any()
+    n = 5 if name == "c5" else 3
+    check_sampled_groups(spec, b, out, n_groups=n, n_heads=2)
+    if name == "c5":  # the first and the last group too (queue head / tail)
+        check_sampled_groups(spec.subset([0, spec.G - 1]), _group_batch(b, [0, spec.G - 1]),
+                             _group_rows(b, out, [0, spec.G - 1]), n_groups=2, n_heads=8)
+
+
+def _group_rows(b, out, groups):
+    return torch.cat([out[int(b["cu_q"][b["cu_req"][g]]):int(b["cu_q"][b["cu_req"][g + 1]])]
+                      for g in groups])
+
+
+def _group_batch(b, groups):
+    """Sub-batch of whole groups (device tensor slices + rebased offsets)."""
+    def cat(t, cu, idx):
+        return torch.cat([t[int(cu[i]):int(cu[i + 1])] for i in idx])
+    reqs = [r for g in groups for r in range(int(b["cu_req"][g]), int(b["cu_req"][g + 1]))]
+    cum = lambda lens: np.concatenate([[0], np.cumsum(lens)]).astype(np.int64)  # noqa: E731
+    return dict(q=cat(b["q"], b["cu_q"], reqs), k_prefix=cat(b["k_prefix"], b["cu_prefix"], groups),
+                v_prefix=cat(b["v_prefix"], b["cu_prefix"], groups),
+                k_distinct=cat(b["k_distinct"], b["cu_distinct"], reqs),
+                v_distinct=cat(b["v_distinct"], b["cu_distinct"], reqs),
+                cu_req=cum([int(b["cu_req"][g + 1] - b["cu_req"][g]) for g in groups]),
+                cu_q=cum([int(b["cu_q"][r + 1] - b["cu_q"][r]) for r in reqs]),
+                cu_prefix=cum([int(b["cu_prefix"][g + 1] - b["cu_prefix"][g]) for g in groups]),
+                cu_distinct=cum([int(b["cu_distinct"][r + 1] - b["cu_distinct"][r]) for r in reqs]))
 
 
 def group_host_slice(b: dict, g: int) -> dict:

@@ -28,8 +28,8 @@ def test_shards_reassemble_to_the_single_launch(name, world):
     out = torch.full_like(full, float("nan"))
     for s in shards:
         if s.num_tokens:
-            local = D.run_local(s, b["q"], b["k_prefix"], b["v_prefix"], b["k_distinct"],
-                                b["v_distinct"], spec.Hkv)
+            local = D.run_local(s, *D.select_shard(s, b["q"], b["k_prefix"], b["v_prefix"],
+                                                   b["k_distinct"], b["v_distinct"]), spec.Hkv)
             out.index_copy_(0, torch.as_tensor(s.token_rows, device="cuda"), local)
     torch.cuda.synchronize()
     assert not torch.isnan(out).any()

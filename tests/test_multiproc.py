@@ -107,26 +107,23 @@ def test_gloo_world2_group_sharding():
                 assert np.abs(np.array(a) - w).max() < 1e-12
 
 
-def test_bench_rank_specs_weak_and_strong():
+def test_bench_rank_groups_strong_sharding():
     import importlib.util
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
     spec_ = importlib.util.spec_from_file_location("bench", os.path.join(root, "bench.py"))
     bench = importlib.util.module_from_spec(spec_)
     spec_.loader.exec_module(bench)
-    # c2 weak scaling: each rank gets its own 16 groups with distinct global ids
-    ids = set()
-    for r in range(4):
-        s, scaling = bench.rank_spec("c2", r, 4)
-        assert scaling == "weak" and s.G == 16
-        ids |= set(s.group_ids)
-    assert len(ids) == 64
-    # c5 strong scaling: LPT shards cover the 1024 groups exactly once
-    seen = []
-    for r in range(8):
-        s, scaling = bench.rank_spec("c5", r, 8)
-        assert scaling == "strong"
-        seen += s.group_ids
-    assert sorted(seen) == list(range(1024))
+    assert bench.DEFAULT_CONFIG == "c5"
+    # every config is strong-scaled: LPT shards cover the groups exactly once
+    for name, world in (("c5", 8), ("c4", 4), ("c2", 2)):
+        full = W.config(name)
+        seen = []
+        for r in range(world):
+            seen += bench.rank_groups(full, r, world)
+        assert sorted(seen) == list(range(full.G))
+    # the config dict is the workload identity, identical for both arms
+    c = bench.config_dict(W.config("c5"), 1)
+    assert c["workload"] == "c5" and c["groups"] == 1024 and c["tokens"] == 65536
 
 
 def _gather_worker(rank, world, port, q):
@@ -143,11 +140,14 @@ def _gather_worker(rank, world, port, q):
         s = shards[rank]
         host = {k: b[k].double().numpy() for k in ("q", "k_prefix", "v_prefix", "k_distinct",
                                                      "v_distinct")}
-        local = S.packed_attention(host["q"][s.token_rows], host["k_prefix"][s.prefix_rows],
-                                   host["v_prefix"][s.prefix_rows],
-                                   host["k_distinct"][s.distinct_rows],
-                                   host["v_distinct"][s.distinct_rows], s.cu_req, s.cu_q,
-                                   s.cu_prefix, s.cu_distinct, spec.Hq, spec.Hkv)
+        if s.num_groups:
+            local = S.packed_attention(host["q"][s.token_rows], host["k_prefix"][s.prefix_rows],
+                                       host["v_prefix"][s.prefix_rows],
+                                       host["k_distinct"][s.distinct_rows],
+                                       host["v_distinct"][s.distinct_rows], s.cu_req, s.cu_q,
+                                       s.cu_prefix, s.cu_distinct, spec.Hq, spec.Hkv)
+        else:  # more ranks than groups: the empty shard still joins the gather
+            local = np.zeros((0, spec.Hq, spec.dv))
         full = D.gather_outputs(torch.as_tensor(local), shards, rank)
         if rank == 0:
             ref = S.packed_attention(host["q"], host["k_prefix"], host["v_prefix"],
@@ -159,19 +159,79 @@ def _gather_worker(rank, world, port, q):
         dist.destroy_process_group()
 
 
-@pytest.mark.timeout(300)
-def test_gloo_world2_shard_run_and_output_gather():
+def _spawn(target, world, *extra):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_gather_worker, args=(r, 2, port, q)) for r in range(2)]
+    procs = [ctx.Process(target=target, args=(r, world, port, q) + extra) for r in range(world)]
     for p in procs:
         p.start()
-    err = q.get(timeout=240)
+    res = q.get(timeout=240)
     for p in procs:
         p.join(timeout=60)
         assert p.exitcode == 0
-    assert err == 0.0
+    return res
+
+
+@pytest.mark.timeout(300)
+def test_gloo_world2_shard_run_and_output_gather():
+    assert _spawn(_gather_worker, 2) == 0.0
+
+
+@pytest.mark.timeout(300)
+def test_gloo_more_ranks_than_groups_gather():
+    """world > G: empty shards still join the collective (no hang), output exact."""
+    assert _spawn(_gather_worker, _small_skewed().G + 1) == 0.0
+
+
+def _slab_worker(rank, world, port, q, num_slabs):
+    """SlabGather: per-slab compute (oracle stand-in) + per-slab all_gather, then the
+    reassembled output equals the single-process oracle."""
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2412_03594_b200 import distributed as D
+        spec = _small_skewed()
+        off = W.offsets(spec)
+        shards = D.shard(off["cu_req"], off["cu_q"], off["cu_prefix"], off["cu_distinct"],
+                         spec.Hq, spec.Hkv, spec.d, spec.dv, spec.torch_dtype, world)
+        me = shards[rank]
+        sub = spec.subset(me.groups.tolist())
+        b = W.make_batch(sub, "cpu")   # only this rank's groups (per-group seeds)
+        host = {k: b[k].double().numpy() for k in ("q", "k_prefix", "v_prefix", "k_distinct",
+                                                     "v_distinct")}
+        sg = D.SlabGather(shards, rank, num_slabs, (spec.Hq, spec.dv), torch.float64, "cpu")
+        calls = []
+
+        def compute(i, out_rows):
+            g0, g1 = sg.slab_groups(i)
+            calls.append((g0, g1))
+            res = S.packed_attention(host["q"], host["k_prefix"], host["v_prefix"],
+                                     host["k_distinct"], host["v_distinct"], b["cu_req"],
+                                     b["cu_q"], b["cu_prefix"], b["cu_distinct"], spec.Hq,
+                                     spec.Hkv, groups=range(g0, g1))
+            t0, t1 = int(b["cu_q"][b["cu_req"][g0]]), int(b["cu_q"][b["cu_req"][g1]])
+            out_rows.copy_(torch.as_tensor(res[t0:t1]))
+
+        sg.run(compute)
+        full = sg.result()
+        assert sum(g1 - g0 for g0, g1 in calls) == me.num_groups
+        if rank == 0:
+            fb = W.make_batch(spec, "cpu")
+            fh = {k: fb[k].double().numpy() for k in ("q", "k_prefix", "v_prefix", "k_distinct",
+                                                        "v_distinct")}
+            ref = S.packed_attention(fh["q"], fh["k_prefix"], fh["v_prefix"], fh["k_distinct"],
+                                     fh["v_distinct"], fb["cu_req"], fb["cu_q"], fb["cu_prefix"],
+                                     fb["cu_distinct"], spec.Hq, spec.Hkv)
+            q.put(float(np.abs(full.numpy() - ref).max()))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.timeout(300)
+@pytest.mark.parametrize("world,num_slabs", [(2, 3), (3, 2)])
+def test_gloo_slab_gather_overlapped_output(world, num_slabs):
+    assert _spawn(_slab_worker, world, num_slabs) < 1e-12
 
 
 def test_shard_edge_cases_on_host():
