@@ -339,6 +339,9 @@ psa_status psa_run(const psa_problem* prob, const psa_plan* pl, void* ws, size_t
     // CTAs without a tile item move on to the VEC queue at once.
     const int grid = pl->num_sms * pl->ctas_per_sm;
     int nt = pl->plan.num_tile_items > 0 ? grid : 0;
+    if (pl->use_v2 && pl->plan.num_tile_items > 0) nt = pl->plan.tile_ctas;
+    if (const char* e = std::getenv("PSA_TILE_CTAS"))  // diagnostics: override the split
+      nt = std::max(0, std::min(grid, std::atoi(e)));
     k.n_tile_ctas = nt;
   }
   k.Hq = in.Hq; k.Hkv = in.Hkv; k.gqa = in.Hq / in.Hkv; k.d = in.d; k.dv = in.dv;

@@ -82,6 +82,11 @@ struct alignas(16) Shared {
   int item_idx[2];
   float red[2][4][kR];  // per-warp partial row maxima (double-buffered by block parity) / sums
   int item_fast[2];     // producer's fast-merge decision per item slot (see NoFast)
+  // Item metadata staged by the producer (it already holds the record one item ahead),
+  // so the softmax warps start an item without dependent global round trips.
+  alignas(16) int32_t item_rec[2][16];  // the ItemRec
+  int64_t item_tok0[2];                 // first token of the item's group
+  int item_other[2];                    // fast merge: workspace row of the other contribution
   // merge queue: softmax thread 0 appends the units this CTA completes, warps 6-7 merge them
   dev::MergeQueue mq;
 };
@@ -191,14 +196,15 @@ __device__ __forceinline__ int block_nvalid(const ItemT& it, int nbA, int j) {
 // `fast` (see psa_kernel.cu, DecFast): an item whose only merge unit has one other
 // contributor that already arrived (typically the group's prefix tile) merges that
 // contributor's partial in registers and writes the final rows itself — no partial
-// rows, no arrival task, no merge. fast.probe(it) (thread 0) / fast.fetch(it, t, R,
-// Other&) (all threads, after block 0's barrier) / fast.finish(it, t, R, m, L, ov, o).
+// rows, no arrival task, no merge. fast.probe(it, other_row) (producer lane 0; sets the
+// workspace row of the other contribution) / fast.fetch(other_row, t, R, Other&) (all
+// threads, at the item start) / fast.finish(it, tok0, t, R, m, L, ov, o).
 struct NoFast {
   struct Other {};
-  template <typename I> __device__ int probe(const I&) const { return 0; }
-  template <typename I> __device__ void fetch(const I&, int, int, Other&) const {}
+  template <typename I> __device__ int probe(const I&, int&) const { return 0; }
+  __device__ void fetch(int, int, int, Other&) const {}
   template <typename I>
-  __device__ void finish(const I&, int, int, const float (&)[kR], const float (&)[kR],
+  __device__ void finish(const I&, int64_t, int, int, const float (&)[kR], const float (&)[kR],
                          const float (&)[kR], const Other&) const {}
 };
 
@@ -233,8 +239,8 @@ __device__ void run(const KParams& p, uint8_t* smem_raw, Shared* sh, uint32_t tm
     uint32_t c = 0;  // K/V slot loads issued
     for (uint32_t k = 0;; ++k) {
       const uint32_t q = k & 1;
-      int fast_k = 0;
-      if (lane == 0 && idx < n_items) fast_k = fast.probe(it);  // latency overlaps the wait
+      int fast_k = 0, other_k = -1;
+      if (lane == 0 && idx < n_items) fast_k = fast.probe(it, other_k);  // latency overlaps the wait
       dev::mbar_wait(&sh->item_empty[q], ((k >> 1) & 1) ^ 1);
       if (idx >= n_items) {
         if (lane == 0) {
@@ -271,6 +277,10 @@ __device__ void run(const KParams& p, uint8_t* smem_raw, Shared* sh, uint32_t tm
       if (lane == 0) {
         sh->item_idx[q] = idx;
         sh->item_fast[q] = fast_k;
+        sh->item_other[q] = other_k;
+        sh->item_tok0[q] = tok0;
+        static_assert(sizeof(it) <= sizeof(sh->item_rec[0]), "item record too large");
+        *reinterpret_cast<decltype(load_item_at(0))*>(sh->item_rec[q]) = it;
         if (q_tma) {
           const int t0 = int(tok0 + it.row0 / p.gqa);
           dev::mbar_arrive_expect_tx(&sh->item_full[q], uint32_t(kQBytes));
@@ -422,16 +432,16 @@ __device__ void run(const KParams& p, uint8_t* smem_raw, Shared* sh, uint32_t tm
       }
       long long t_item0 = 0;
       if (p.trace_cap > 0 && t == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_item0));
-      const auto it = load_item_at(idx);
-      int nbA, nb;
-      int64_t pbase, dbase;
-      item_blocks(p, it, nbA, nb, pbase, dbase);
+      const auto it = *reinterpret_cast<const decltype(load_item_at(0))*>(sh->item_rec[q]);
+      const int64_t it_tok0 = sh->item_tok0[q];
+      const int nbA = (it.pk1 - it.pk0 + kBK - 1) / kBK;
+      const int nb = nbA + (it.dk1 - it.dk0 + kBK - 1) / kBK;
       const int R = it.nrows;
       // fast merge decided by the producer (its acquire load + this item_full wait order
       // the other contributor's partial rows before the fetch); fetched now, used at the end
       const bool fast_on = sh->item_fast[q] != 0;
       typename Fast::Other other;
-      if (fast_on) fast.fetch(it, t, R, other);
+      if (fast_on) fast.fetch(sh->item_other[q], t, R, other);
       // rows >= R keep m = 0 and x = -inf: their exps are exactly 0, no NaN, and
       // every row's arithmetic stays branch-free (the rows interleave for ILP).
       float m[kR], lp[kR];
@@ -443,11 +453,10 @@ __device__ void run(const KParams& p, uint8_t* smem_raw, Shared* sh, uint32_t tm
 #pragma unroll
       for (int r = 0; r < kR; ++r) { limp[r] = INT_MAX; limd[r] = INT_MAX; }
       if constexpr (causal) {
-        const int64_t tok0 = __ldg(p.group_tok0 + it.g);
 #pragma unroll
         for (int r = 0; r < kR; ++r) {
           if (r < R) {
-            const int64_t tok = tok0 + (it.row0 + r) / p.gqa;
+            const int64_t tok = it_tok0 + (it.row0 + r) / p.gqa;
             limp[r] = __ldg(p.tok_lim + tok * 2);
             limd[r] = __ldg(p.tok_lim + tok * 2 + 1);
           }
@@ -476,9 +485,7 @@ __device__ void run(const KParams& p, uint8_t* smem_raw, Shared* sh, uint32_t tm
           v[r] = x[r];
         }
 #pragma unroll
-        for (int o = 16; o > 0; o >>= 1)
-#pragma unroll
-          for (int r = 0; r < kR; ++r) v[r] = fmaxf(v[r], __shfl_xor_sync(0xffffffffu, v[r], o));
+        for (int r = 0; r < kR; ++r) v[r] = dev::warp_max_f32(v[r]);  // one CREDUX.MAX.F32 per row
         if (lane == 0) {
 #pragma unroll
           for (int r = 0; r < kR; ++r) sh->red[g & 1][warp][r] = v[r];
@@ -574,8 +581,8 @@ __device__ void run(const KParams& p, uint8_t* smem_raw, Shared* sh, uint32_t tm
       float ov[kR];
 #pragma unroll
       for (int r = 0; r < kR; ++r) ov[r] = __uint_as_float(o[r]);
-      if (fast_on) fast.finish(it, t, R, m, L, ov, other);  // merged in registers: final rows
-      else finish(it, idx, t, R, m, L, ov);  // output, or partial rows queued for arrival
+      if (fast_on) fast.finish(it, it_tok0, t, R, m, L, ov, other);  // merged in registers: final rows
+      else finish(it, it_tok0, idx, t, R, m, L, ov);  // output, or partial rows queued for arrival
       if (t == 0) dbg(p, 9, g - 1);
       named_sync_softmax(pi);      // red[] reuse + item slot release after everyone finished
       if (t == 0) dev::mbar_arrive(&sh->item_empty[q]);

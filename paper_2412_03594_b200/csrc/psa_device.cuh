@@ -234,6 +234,23 @@ __host__ __device__ constexpr uint32_t umma_idesc_f16(uint32_t ab_format, uint32
 // fence.sc.gpu behind __threadfence()); paired with relaxed atomics it forms the
 // release / acquire patterns of the PTX memory model.
 __device__ __forceinline__ void fence_acq_rel_gpu() { asm volatile("fence.acq_rel.gpu;" ::: "memory"); }
+// Warp-wide max of a float (sm_100a CREDUX.MAX.F32; NaN inputs are ignored like fmaxf's).
+__device__ __forceinline__ float warp_max_f32(float v) {
+  float r;
+  asm volatile("redux.sync.max.f32 %0, %1, 0xffffffff;" : "=f"(r) : "f"(v));
+  return r;
+}
+// Coherent-at-L2 load issued where it is written (volatile: not sunk to its use).
+__device__ __forceinline__ float ld_cg_f32(const float* p) {
+  float v;
+  asm volatile("ld.global.cg.f32 %0, [%1];" : "=f"(v) : "l"(p));
+  return v;
+}
+__device__ __forceinline__ float2 ld_cg_f32x2(const float2* p) {
+  float2 v;
+  asm volatile("ld.global.cg.v2.f32 {%0, %1}, [%2];" : "=f"(v.x), "=f"(v.y) : "l"(p));
+  return v;
+}
 
 // ---- CTA-local merge queue ------------------------------------------------------
 // Bounded MPMC ring in shared memory: threads that complete work push tasks, merge

@@ -747,38 +747,43 @@ struct DecFast {
     float m[dec::kR], l[dec::kR], o[dec::kR];
     int first;  // the other contribution precedes this item's in contribution order
   };
-  __device__ int probe(const ItemRec& it) const {
-    if (it.ws_row < 0 || it.u1 - it.u0 != 1) return 0;
+  // Producer lane 0. Returns 1 (fast) with `other` = (workspace row of the other
+  // contribution) * 2 + (the other contribution comes first in contribution order).
+  __device__ int probe(const ItemRec& it, int& other) const {
+    if (!p.dec_fast || it.ws_row < 0 || it.u1 - it.u0 != 1) return 0;
     const int32_t* U = p.units + (int64_t)it.u0 * kUnitWords;
     if (__ldg(U + kUnRows) != it.nrows || __ldg(U + kUnContribCount) != 2 ||
         __ldg(U + kUnRow0) != it.row0)
       return 0;
-    int cnt;
-    asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(cnt) : "l"(p.unit_cnt + it.u0) : "memory");
-    return cnt == 1 ? 1 : 0;
-  }
-  __device__ void fetch(const ItemRec& it, int t, int R, Other& o) const {
-    const int32_t* U = p.units + (int64_t)it.u0 * kUnitWords;
     const int cb = __ldg(U + kUnContribBegin);
     const int c0 = __ldg(p.contribs + cb), c1 = __ldg(p.contribs + cb + 1);
-    o.first = c0 != it.ws_row;
-    const int64_t base = o.first ? c0 : c1;
+    int cnt;
+    asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(cnt) : "l"(p.unit_cnt + it.u0) : "memory");
+    if (cnt != 1) return 0;
+    const int first = c0 != it.ws_row;
+    other = (first ? c0 : c1) * 2 + first;
+    return 1;
+  }
+  // All softmax threads at the item start (ordered after the producer's acquire by the
+  // item barrier); the loads are issued here and consumed by finish().
+  __device__ void fetch(int other, int t, int R, Other& o) const {
+    o.first = other & 1;
+    const int64_t base = other >> 1;
     const float* WO = static_cast<const float*>(p.ws_o);
     const float2* WML = static_cast<const float2*>(p.ws_ml);
 #pragma unroll
     for (int r = 0; r < dec::kR; ++r) {
       if (r < R) {
-        const float2 ml = __ldcg(WML + base + r);
+        const float2 ml = dev::ld_cg_f32x2(WML + base + r);
         o.m[r] = ml.x;
         o.l[r] = ml.y;
-        o.o[r] = __ldcg(WO + (base + r) * 128 + t);
+        o.o[r] = dev::ld_cg_f32(WO + (base + r) * 128 + t);
       }
     }
   }
-  __device__ void finish(const ItemRec& it, int t, int R, const float (&m)[dec::kR],
+  __device__ void finish(const ItemRec& it, int64_t tok0, int t, int R, const float (&m)[dec::kR],
                          const float (&L)[dec::kR], const float (&ov)[dec::kR],
                          const Other& o) const {
-    const int64_t tok0 = __ldg(p.group_tok0 + it.g);
     const bool partial_out = p.flags & PSA_FLAG_PARTIAL_OUT;
 #pragma unroll
     for (int r = 0; r < dec::kR; ++r) {
@@ -817,7 +822,8 @@ struct DecFast {
 // partial rows + arrival at the merge units, or the final output.
 template <typename T>
 __device__ __forceinline__ void dec_finish(const KParams& p, dec::Shared* sh, const ItemRec& it,
-                                           int idx, int t, int R, const float (&m)[dec::kR],
+                                           int64_t tok0, int idx, int t, int R,
+                                           const float (&m)[dec::kR],
                                            const float (&L)[dec::kR], const float (&ov)[dec::kR],
                                            int pi) {
   if (it.ws_row >= 0) {
@@ -837,7 +843,6 @@ __device__ __forceinline__ void dec_finish(const KParams& p, dec::Shared* sh, co
     if (t == 0) dec::enqueue_merge(sh, idx);
     return;
   }
-  const int64_t tok0 = __ldg(p.group_tok0 + it.g);
   const bool partial_out = p.flags & PSA_FLAG_PARTIAL_OUT;
 #pragma unroll
   for (int r = 0; r < dec::kR; ++r) {
@@ -973,9 +978,9 @@ __global__ void __launch_bounds__(kThreads, 2) psa_persistent(const __grid_const
     };
     auto dec_phase = [&]() {
       auto load_at = [&](int idx) { return load_item(p.items + (int64_t)idx * kItemWords); };
-      auto finish = [&](const ItemRec& it, int idx, int t, int R, const float (&m)[dec::kR],
+      auto finish = [&](const ItemRec& it, int64_t tok0, int idx, int t, int R, const float (&m)[dec::kR],
                         const float (&L)[dec::kR], const float (&ov)[dec::kR]) {
-        dec_finish<T>(p, &s_dec, it, idx, t, R, m, L, ov, 0);
+        dec_finish<T>(p, &s_dec, it, tok0, idx, t, R, m, L, ov, 0);
       };
       auto arrive = [&](int idx) {
         warp_arrive_rows(p, load_at(idx), INT_MIN, INT_MAX,
@@ -1136,9 +1141,9 @@ __global__ void __launch_bounds__(kV2Threads, 1) psa_v2(const __grid_constant__ 
   if (p.use_dec && (warp >> 3) < p.dec_pipes) {
     const int pi = warp >> 3;
     const size_t half = dec::pipe_stride(p.dec_slots);
-    auto finish = [&](const ItemRec& it, int idx, int t, int R, const float (&m)[dec::kR],
+    auto finish = [&](const ItemRec& it, int64_t tok0, int idx, int t, int R, const float (&m)[dec::kR],
                       const float (&L)[dec::kR], const float (&ov)[dec::kR]) {
-      dec_finish<T>(p, &s_dec[pi], it, idx, t, R, m, L, ov, pi);
+      dec_finish<T>(p, &s_dec[pi], it, tok0, idx, t, R, m, L, ov, pi);
     };
     dec::run<T, kCausal>(p, smem + pi * half, &s_dec[pi], tmem + 64u * uint32_t(pi), pi, load_at, finish,
                 arrive_dec, DecFast<T>{p});
@@ -1272,6 +1277,7 @@ int launch_v2(const KParams& p_in, int32_t num_sms, void* stream) {
   const int dbg = dbg_env ? std::atoi(dbg_env) : 0;
   p.dec_pipes = (dbg & 1) ? 1 : 2;
   p.tile_pp = (dbg & 32) ? 0 : 1;
+  p.dec_fast = (dbg & 256) ? 0 : 1;
   const char* dbg_cta = std::getenv("PSA_DBG_CTA");
   p.dbg_cta = dbg_cta ? std::atoi(dbg_cta) : 0;
   if (dbg & 2) p.dec_slots = 2;

@@ -335,6 +335,7 @@ std::string build_plan(const PlanInput& in, const PlanOptions& opt, Plan* out) {
   out->num_items = int32_t(items.size());
   out->num_units = int32_t(units.size());
   out->workspace_rows = ws;
+  out->tile_ctas = out->num_tile_items > 0 ? int32_t(ctas) : 0;
   return "";
 }
 

@@ -69,6 +69,7 @@ struct Plan {
   int64_t workspace_rows = 0;
   int32_t chunk_keys = 0;
   int64_t tile_cost = 0, total_cost = 0;  // LPT cost model totals (host heuristics only)
+  int32_t tile_ctas = 0;  // v2: CTAs that start on the TILE queue (the rest on decode)
 };
 
 // Returns "" on success, else the validation message (maps to PSA_INVALID_ARGUMENT).

@@ -86,6 +86,13 @@ def config(name: str) -> Spec:
     if name == "c2_decode":
         return Spec("c2_decode", 32, 8, 128, 128, "bf16", "normal", [0] * 16,
                     [[(1, 256)] * 32 for _ in range(16)], seed=2)
+    # diagnostic halves of c5
+    if name == "c5_prefix":
+        return Spec("c5_prefix", 32, 8, 128, 128, "bf16", "normal", [4096] * 1024,
+                    [[(1, 0)] * 64 for _ in range(1024)], seed=5)
+    if name == "c5_decode":
+        return Spec("c5_decode", 32, 8, 128, 128, "bf16", "normal", [0] * 1024,
+                    [[(1, 256)] * 64 for _ in range(1024)], seed=5)
     # diagnostic parts of c3: the prefix tiles alone / the prefill chunks' own KV alone
     if name == "c3_prefix":
         reqs = [(1, 0)] * 16 + [(512, 0)] + [(1, 0)] * 16 + [(512, 0)]

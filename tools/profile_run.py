@@ -13,6 +13,7 @@ from paper_2412_03594_b200 import workloads as W  # noqa: E402
 ap = argparse.ArgumentParser()
 ap.add_argument("--config", default="c2")
 ap.add_argument("--ctas-per-sm", type=int, default=0)
+ap.add_argument("--num-sms", type=int, default=0)
 ap.add_argument("--warmup", type=int, default=3)
 ap.add_argument("--iters", type=int, default=1)
 args = ap.parse_args()
@@ -21,7 +22,7 @@ spec = W.config(args.config)
 b = W.make_batch(spec, dev)
 op = P.PrefixSharedAttention(b["cu_req"], b["cu_q"], b["cu_prefix"], b["cu_distinct"], spec.Hq,
                              spec.Hkv, spec.d, spec.dv, spec.torch_dtype, dev,
-                                 options=P.PlanOptions(ctas_per_sm=args.ctas_per_sm))
+                                 options=P.PlanOptions(ctas_per_sm=args.ctas_per_sm, num_sms=args.num_sms))
 ins = (b["q"], b["k_prefix"], b["v_prefix"], b["k_distinct"], b["v_distinct"])
 for _ in range(args.warmup + args.iters):
     op(*ins)
