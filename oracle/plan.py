@@ -16,7 +16,7 @@ import numpy as np
 ITEM_WORDS = 16
 UNIT_WORDS = 8
 (IT_KIND, IT_GROUP, IT_HEAD, IT_ROW0, IT_ROWS, IT_REQUEST, IT_PK0, IT_PK1, IT_DK0, IT_DK1,
- IT_UNIT0, IT_UNIT1, IT_WSROW, IT_CANON) = range(14)
+ IT_UNIT0, IT_UNIT1, IT_WSROW, IT_CANON, IT_PAIR) = range(15)
 (UN_GROUP, UN_HEAD, UN_ROW0, UN_ROWS, UN_CBEGIN, UN_CCOUNT) = range(6)
 KIND_VEC, KIND_TILE = 0, 1
 TILE_M = 128
@@ -238,6 +238,19 @@ def build_plan(G, R, Hq, Hkv, d, dv, dtype, cu_req, cu_q, cu_prefix, cu_distinct
             it = items[i]
             contribs.append(-1 if it[IT_WSROW] < 0 else it[IT_WSROW] + (rec[UN_ROW0] - it[IT_ROW0]))
 
+    # pair merges (psa_plan.cpp, before step 4): one of exactly two contributors of one
+    # unit spanning the item's rows -> other contribution's ws row * 2 + (it comes first)
+    for it in items:
+        pair = -1
+        if it[IT_WSROW] >= 0 and it[IT_UNIT1] - it[IT_UNIT0] == 1:
+            u = units[it[IT_UNIT0]]
+            if u[UN_ROW0] == it[IT_ROW0] and u[UN_ROWS] == it[IT_ROWS] and u[UN_CCOUNT] == 2:
+                c0, c1 = contribs[u[UN_CBEGIN]], contribs[u[UN_CBEGIN] + 1]
+                first = c0 != it[IT_WSROW]
+                pair = (c0 if first else c1) * 2 + (1 if first else 0)
+                if pair > 2**31 - 1:
+                    pair = -1
+        it[IT_PAIR] = pair
     cost = []
     for it in items:
         keys = (it[IT_PK1] - it[IT_PK0]) + (it[IT_DK1] - it[IT_DK0])

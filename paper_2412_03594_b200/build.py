@@ -48,6 +48,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
     cmd = [nvcc(), *ARCH, "-O3", "-std=c++17", "-lineinfo", "-shared", "-Xcompiler", "-fPIC",
            "-cudart", "static", "-Xptxas", "-v" if verbose else "-O3",
            "-I", os.path.join(ROOT, "include"),
+           *(["-DPSA_TRACE_EVENTS"] if os.environ.get("PSA_TRACE_EVENTS") == "1" else []),
            *[os.path.join(CSRC, s) for s in SOURCES], "-o", LIB + ".tmp"]
     res = subprocess.run(cmd, capture_output=True, text=True)
     if res.returncode != 0:

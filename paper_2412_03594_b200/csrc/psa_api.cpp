@@ -345,6 +345,9 @@ psa_status psa_run(const psa_problem* prob, const psa_plan* pl, void* ws, size_t
     k.n_tile_ctas = nt;
   }
   k.Hq = in.Hq; k.Hkv = in.Hkv; k.gqa = in.Hq / in.Hkv; k.d = in.d; k.dv = in.dv;
+  k.gqa_shift = -1;
+  for (int sh = 0; sh < 31; ++sh)
+    if ((1 << sh) == k.gqa) k.gqa_shift = sh;
   k.flags = prob->flags;
   // scale == 0 (uniform weights; allowed by naive_attention, attention.py:135-136): the
   // softmaxes mask a key by setting its raw score to -inf before scaling, and -inf * 0

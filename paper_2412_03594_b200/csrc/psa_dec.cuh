@@ -55,6 +55,12 @@ __device__ __forceinline__ void load_kv_block(const KParams& p, uint8_t* dst, co
   }
 }
 
+// Output row (token * Hq + query head) of stacked row `row` of kv head h.
+__device__ __forceinline__ int64_t out_index(const KParams& p, int64_t tok0, int h, int row) {
+  const int tq = p.gqa_shift >= 0 ? row >> p.gqa_shift : row / p.gqa;
+  return (tok0 + tq) * p.Hq + (int64_t)h * p.gqa + (row - tq * p.gqa);
+}
+
 namespace dec {
 
 constexpr int kBK = 128;               // keys per block (MMA M)
@@ -87,6 +93,7 @@ struct alignas(16) Shared {
   alignas(16) int32_t item_rec[2][16];  // the ItemRec
   int64_t item_tok0[2];                 // first token of the item's group
   int item_other[2];                    // fast merge: workspace row of the other contribution
+  int64_t item_oidx[2][kR];             // output row (token * Hq + query head) of each item row
   // merge queue: softmax thread 0 appends the units this CTA completes, warps 6-7 merge them
   dev::MergeQueue mq;
 };
@@ -138,7 +145,7 @@ __device__ __forceinline__ void merge_loop(const KParams& p, Shared* sh, MergeUn
 // Diagnostics: clock64 of per-block events of CTA 0's first 64 decode blocks, after
 // the tile events (psa_debug_set_trace). Slot = (16 + event) * 64 + global block.
 __device__ __forceinline__ void dbg(const KParams& p, int ev, uint32_t g) {
-  if (p.trace_cap > 0 && int(blockIdx.x) == p.dbg_cta && g < 64) {
+  if (kTraceEvents && p.trace_cap > 0 && int(blockIdx.x) == p.dbg_cta && g < 64) {
     long long t;
     asm volatile("mov.u64 %0, %%clock64;" : "=l"(t));
     p.trace[(int64_t(p.num_items) + 4096) * 4 + (16 + ev) * 64 + g] = t;
@@ -198,13 +205,13 @@ __device__ __forceinline__ int block_nvalid(const ItemT& it, int nbA, int j) {
 // contributor's partial in registers and writes the final rows itself — no partial
 // rows, no arrival task, no merge. fast.probe(it, other_row) (producer lane 0; sets the
 // workspace row of the other contribution) / fast.fetch(other_row, t, R, Other&) (all
-// threads, at the item start) / fast.finish(it, tok0, t, R, m, L, ov, o).
+// threads, at the item start) / fast.finish(it, oidx, t, R, m, L, ov, o).
 struct NoFast {
   struct Other {};
   template <typename I> __device__ int probe(const I&, int&) const { return 0; }
   __device__ void fetch(int, int, int, Other&) const {}
   template <typename I>
-  __device__ void finish(const I&, int64_t, int, int, const float (&)[kR], const float (&)[kR],
+  __device__ void finish(const I&, const int64_t*, int, int, const float (&)[kR], const float (&)[kR],
                          const float (&)[kR], const Other&) const {}
 };
 
@@ -265,6 +272,8 @@ __device__ void run(const KParams& p, uint8_t* smem_raw, Shared* sh, uint32_t tm
         dev::fence_proxy_async_smem();
         __syncwarp();
       }
+      if (lane < kR && lane < it.nrows) sh->item_oidx[q][lane] = out_index(p, tok0, it.h, it.row0 + lane);
+      __syncwarp();  // ordered before lane 0's item_full arrival
       // next item: its index (claimed one iteration ago) and its record
       const int next = __shfl_sync(0xffffffffu, raw, 0);
       if (lane == 0 && next < n_items) raw = p.n_tile_items + atomicAdd(&p.ctrl->next_vec, 1);
@@ -426,6 +435,7 @@ __device__ void run(const KParams& p, uint8_t* smem_raw, Shared* sh, uint32_t tm
       const uint32_t q = k & 1, b = k & 1;
       dev::mbar_wait(&sh->item_full[q], (k >> 1) & 1);
       const int idx = sh->item_idx[q];
+      if (t == 0) dbg(p, 25, g);
       if (idx < 0) {
         if (t == 0) dev::mq_close(&sh->mq);
         break;
@@ -442,6 +452,7 @@ __device__ void run(const KParams& p, uint8_t* smem_raw, Shared* sh, uint32_t tm
       const bool fast_on = sh->item_fast[q] != 0;
       typename Fast::Other other;
       if (fast_on) fast.fetch(sh->item_other[q], t, R, other);
+      if (t == 0) dbg(p, 26, g);
       // rows >= R keep m = 0 and x = -inf: their exps are exactly 0, no NaN, and
       // every row's arithmetic stays branch-free (the rows interleave for ILP).
       float m[kR], lp[kR];
@@ -578,11 +589,13 @@ __device__ void run(const KParams& p, uint8_t* smem_raw, Shared* sh, uint32_t tm
       dev::tc_fence_before();
       __syncwarp();
       if (lane == 0) dev::mbar_arrive(&sh->o_empty[b]);
+      if (t == 0) dbg(p, 24, g - 1);
       float ov[kR];
 #pragma unroll
       for (int r = 0; r < kR; ++r) ov[r] = __uint_as_float(o[r]);
-      if (fast_on) fast.finish(it, it_tok0, t, R, m, L, ov, other);  // merged in registers: final rows
-      else finish(it, it_tok0, idx, t, R, m, L, ov);  // output, or partial rows queued for arrival
+      const int64_t* oidx = sh->item_oidx[q];
+      if (fast_on) fast.finish(it, oidx, t, R, m, L, ov, other);  // merged in registers: final rows
+      else finish(it, oidx, idx, t, R, m, L, ov);  // output, or partial rows queued for arrival
       if (t == 0) dbg(p, 9, g - 1);
       named_sync_softmax(pi);      // red[] reuse + item slot release after everyone finished
       if (t == 0) dev::mbar_arrive(&sh->item_empty[q]);

@@ -6,6 +6,14 @@
 #include <cstdint>
 
 namespace psa {
+
+// Per-block clock64 event traces (tools/trace_report.py) cost instruction-cache space
+// on the hot paths: compiled in only with -DPSA_TRACE_EVENTS (PSA_TRACE_EVENTS=1 at build).
+#ifdef PSA_TRACE_EVENTS
+constexpr bool kTraceEvents = true;
+#else
+constexpr bool kTraceEvents = false;
+#endif
 namespace dev {
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {

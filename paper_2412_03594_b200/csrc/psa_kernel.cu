@@ -90,7 +90,7 @@ __device__ __forceinline__ uint64_t globaltimer() {
 }
 
 struct ItemRec {
-  int32_t kind, g, h, row0, nrows, req, pk0, pk1, dk0, dk1, u0, u1, ws_row;
+  int32_t kind, g, h, row0, nrows, req, pk0, pk1, dk0, dk1, u0, u1, ws_row, pair;
 };
 
 __device__ __forceinline__ ItemRec load_item(const int32_t* rec) {
@@ -108,6 +108,7 @@ __device__ __forceinline__ ItemRec load_item(const int32_t* rec) {
   it.u0 = __ldg(rec + kItUnit0);
   it.u1 = __ldg(rec + kItUnit1);
   it.ws_row = __ldg(rec + kItWsRow);
+  it.pair = __ldg(rec + kItPair);
   return it;
 }
 
@@ -583,7 +584,7 @@ __device__ __forceinline__ void merge_chunk_warp(const KParams& p, int u, int r0
 
 // All rows of unit u, by one warp, in chunks of <= 32 (row, contribution) pairs.
 template <typename T>
-__device__ __forceinline__ void merge_unit_warp(const KParams& p, int u) {
+__device__ __noinline__ void merge_unit_warp(const KParams& p, int u) {
   const int32_t* U = p.units + (int64_t)u * kUnitWords;
   const int rows = __ldg(U + kUnRows), cc = __ldg(U + kUnContribCount);
   if (cc > 32) {
@@ -695,7 +696,7 @@ __device__ __forceinline__ void warp_arrive_and_merge(const KParams& p, const It
 // several merge warps share a tile's units). Keeps the gpu-scope fence and the
 // merges off the softmax warps' critical path.
 __device__ __forceinline__ void dbg_clock(const KParams& p, int ev, int slot) {
-  if (slot >= 0 && (threadIdx.x & 31) == 0) {
+  if (kTraceEvents && slot >= 0 && (threadIdx.x & 31) == 0) {
     long long t;
     asm volatile("mov.u64 %0, %%clock64;" : "=l"(t));
     p.trace[(int64_t(p.num_items) + 4096) * 4 + ev * 64 + slot] = t;
@@ -749,19 +750,13 @@ struct DecFast {
   };
   // Producer lane 0. Returns 1 (fast) with `other` = (workspace row of the other
   // contribution) * 2 + (the other contribution comes first in contribution order).
+  // The pair (kItPair) is precomputed by the planner, so this is one acquire load.
   __device__ int probe(const ItemRec& it, int& other) const {
-    if (!p.dec_fast || it.ws_row < 0 || it.u1 - it.u0 != 1) return 0;
-    const int32_t* U = p.units + (int64_t)it.u0 * kUnitWords;
-    if (__ldg(U + kUnRows) != it.nrows || __ldg(U + kUnContribCount) != 2 ||
-        __ldg(U + kUnRow0) != it.row0)
-      return 0;
-    const int cb = __ldg(U + kUnContribBegin);
-    const int c0 = __ldg(p.contribs + cb), c1 = __ldg(p.contribs + cb + 1);
+    if (!p.dec_fast || it.pair < 0) return 0;
     int cnt;
     asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(cnt) : "l"(p.unit_cnt + it.u0) : "memory");
     if (cnt != 1) return 0;
-    const int first = c0 != it.ws_row;
-    other = (first ? c0 : c1) * 2 + first;
+    other = it.pair;
     return 1;
   }
   // All softmax threads at the item start (ordered after the producer's acquire by the
@@ -781,7 +776,7 @@ struct DecFast {
       }
     }
   }
-  __device__ void finish(const ItemRec& it, int64_t tok0, int t, int R, const float (&m)[dec::kR],
+  __device__ void finish(const ItemRec& it, const int64_t* oidx, int t, int R, const float (&m)[dec::kR],
                          const float (&L)[dec::kR], const float (&ov)[dec::kR],
                          const Other& o) const {
     const bool partial_out = p.flags & PSA_FLAG_PARTIAL_OUT;
@@ -798,8 +793,7 @@ struct DecFast {
       const float f1 = l1 > 0.f ? dev::ex2(m1 - M) : 0.f;
       const float Ls = __fadd_rn(__fadd_rn(0.f, __fmul_rn(f0, l0)), __fmul_rn(f1, l1));
       const float O = __fmaf_rn(f1, o1, __fmaf_rn(f0, o0, 0.f));
-      const int row = it.row0 + r;
-      const int64_t idx = (tok0 + row / p.gqa) * p.Hq + (int64_t)it.h * p.gqa + row % p.gqa;
+      const int64_t idx = oidx[r];
       if (partial_out) {
         static_cast<float*>(p.out)[idx * 128 + t] = O;
         if (t == 0) {
@@ -822,7 +816,7 @@ struct DecFast {
 // partial rows + arrival at the merge units, or the final output.
 template <typename T>
 __device__ __forceinline__ void dec_finish(const KParams& p, dec::Shared* sh, const ItemRec& it,
-                                           int64_t tok0, int idx, int t, int R,
+                                           const int64_t* oidx, int idx, int t, int R,
                                            const float (&m)[dec::kR],
                                            const float (&L)[dec::kR], const float (&ov)[dec::kR],
                                            int pi) {
@@ -847,8 +841,7 @@ __device__ __forceinline__ void dec_finish(const KParams& p, dec::Shared* sh, co
 #pragma unroll
   for (int r = 0; r < dec::kR; ++r) {
     if (r < R) {
-      const int row = it.row0 + r;
-      const int64_t idx = (tok0 + row / p.gqa) * p.Hq + (int64_t)it.h * p.gqa + row % p.gqa;
+      const int64_t idx = oidx[r];
       if (partial_out) {
         static_cast<float*>(p.out)[idx * 128 + t] = ov[r];
         if (t == 0) {
@@ -978,9 +971,9 @@ __global__ void __launch_bounds__(kThreads, 2) psa_persistent(const __grid_const
     };
     auto dec_phase = [&]() {
       auto load_at = [&](int idx) { return load_item(p.items + (int64_t)idx * kItemWords); };
-      auto finish = [&](const ItemRec& it, int64_t tok0, int idx, int t, int R, const float (&m)[dec::kR],
+      auto finish = [&](const ItemRec& it, const int64_t* oidx, int idx, int t, int R, const float (&m)[dec::kR],
                         const float (&L)[dec::kR], const float (&ov)[dec::kR]) {
-        dec_finish<T>(p, &s_dec, it, tok0, idx, t, R, m, L, ov, 0);
+        dec_finish<T>(p, &s_dec, it, oidx, idx, t, R, m, L, ov, 0);
       };
       auto arrive = [&](int idx) {
         warp_arrive_rows(p, load_at(idx), INT_MIN, INT_MAX,
@@ -1141,9 +1134,9 @@ __global__ void __launch_bounds__(kV2Threads, 1) psa_v2(const __grid_constant__ 
   if (p.use_dec && (warp >> 3) < p.dec_pipes) {
     const int pi = warp >> 3;
     const size_t half = dec::pipe_stride(p.dec_slots);
-    auto finish = [&](const ItemRec& it, int64_t tok0, int idx, int t, int R, const float (&m)[dec::kR],
+    auto finish = [&](const ItemRec& it, const int64_t* oidx, int idx, int t, int R, const float (&m)[dec::kR],
                       const float (&L)[dec::kR], const float (&ov)[dec::kR]) {
-      dec_finish<T>(p, &s_dec[pi], it, tok0, idx, t, R, m, L, ov, pi);
+      dec_finish<T>(p, &s_dec[pi], it, oidx, idx, t, R, m, L, ov, pi);
     };
     dec::run<T, kCausal>(p, smem + pi * half, &s_dec[pi], tmem + 64u * uint32_t(pi), pi, load_at, finish,
                 arrive_dec, DecFast<T>{p});

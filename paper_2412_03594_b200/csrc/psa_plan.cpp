@@ -285,6 +285,23 @@ std::string build_plan(const PlanInput& in, const PlanOptions& opt, Plan* out) {
     }
   }
 
+  // Pair merges: an item that shares its single unit (spanning exactly its rows) with
+  // one other item can merge that item's partial itself when it arrives last — the
+  // decode pipeline's in-register merge; precomputed so the kernel needs one load.
+  for (auto& it : items) {
+    int64_t pair = -1;
+    if (it[kItWsRow] >= 0 && it[kItUnit1] - it[kItUnit0] == 1) {
+      const auto& u = units[it[kItUnit0]];
+      if (u[kUnRow0] == it[kItRow0] && u[kUnRows] == it[kItRows] && u[kUnContribCount] == 2) {
+        const int32_t c0 = contribs[u[kUnContribBegin]], c1 = contribs[u[kUnContribBegin] + 1];
+        const bool first = c0 != it[kItWsRow];
+        pair = int64_t(first ? c0 : c1) * 2 + (first ? 1 : 0);
+        if (pair > INT32_MAX) pair = -1;
+      }
+    }
+    it[kItPair] = int32_t(pair);
+  }
+
   // 4. LPT queue order: cost descending; ties: tiles by canonical index, VEC items
   //    heads-fastest (below).
   std::vector<int64_t> cost(items.size());

@@ -22,7 +22,9 @@ enum ItemKind : int32_t { kItemVec = 0, kItemTile = 1 };
 enum ItemField : int {
   kItKind = 0, kItGroup, kItHead, kItRow0, kItRows, kItRequest,
   kItPk0, kItPk1, kItDk0, kItDk1, kItUnit0, kItUnit1, kItWsRow, kItCanon,
-  kItReserved0, kItReserved1, kItemWords
+  kItPair,  // one of exactly two contributors of one unit spanning its rows: the other
+            // contribution's workspace row * 2 + (it comes first); else -1
+  kItReserved1, kItemWords
 };
 // Merge-unit record layout (int32 words).
 enum UnitField : int {

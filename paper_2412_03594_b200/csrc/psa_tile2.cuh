@@ -221,7 +221,7 @@ __device__ __forceinline__ void item_shape(const KParams& p, const ItemT& it, in
 // Diagnostics: clock64 of per-block events of CTA 0 (first 64 blocks), slot 0.
 // Slot = event * 64 + block, after the item records (psa_debug_set_trace).
 __device__ __forceinline__ void dbg(const KParams& p, int ev, uint32_t g) {
-  if (p.trace_cap > 0 && int(blockIdx.x) == p.dbg_cta && g < 64) {
+  if (kTraceEvents && p.trace_cap > 0 && int(blockIdx.x) == p.dbg_cta && g < 64) {
     long long t;
     asm volatile("mov.u64 %0, %%clock64;" : "=l"(t));
     p.trace[(int64_t(p.num_items) + 4096) * 4 + ev * 64 + g] = t;

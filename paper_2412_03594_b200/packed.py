@@ -302,6 +302,7 @@ class PrefixSharedAttention:
         self.last_tile_events = out[n:].reshape(-1)[:9 * 64].reshape(9, 64)
         self.last_dec_events = out[n:].reshape(-1)[16 * 64:33 * 64].reshape(17, 64)
         self.last_merge_tasks = out[n:].reshape(-1)[36 * 64:40 * 64].reshape(4, 64)
+        self.last_dec_events2 = out[n:].reshape(-1)[40 * 64:43 * 64].reshape(3, 64)
         self.last_phase = out[self.num_items + 2048:self.num_items + 3072]
         self.last_dec_phase = out[self.num_items + 3072:self.num_items + 4096]
         ctas = out[self.num_items:n]

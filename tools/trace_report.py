@@ -113,6 +113,10 @@ def main():
         names = ["k_issue", "v_issue", "s_issue", "pv_issue", "soft_s_ready", "p_arrive", "item_end", "epi_ofull_wait", "epi_ofull_done", "epi_finish_done", "ld_done", "max_done", "bar1_done", "exp_done", "odone_done", "pstore_done", "fence_done"]
         rep["dec0_events_cycles"] = {nm: [int(x - t0) if x else 0 for x in dv[i, :min(nb, 16)]]
                                      for i, nm in enumerate(names)}
+        d2 = getattr(op, "last_dec_events2", None)
+        if d2 is not None:
+            for i, nm in enumerate(["epi_tmem_ld_done", "item_full_done", "fetch_issued"]):
+                rep["dec0_events_cycles"][nm] = [int(x - t0) if x else 0 for x in d2[i, :min(nb, 16)]]
     ph = getattr(op, "last_phase", None)
     if ph is not None and (ph[:, 3] != 0).any():
         st = tr[:, 2].min()
