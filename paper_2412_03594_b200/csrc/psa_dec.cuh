@@ -182,6 +182,38 @@ __device__ __forceinline__ uint32_t sw128_off(int r, int c, int rows) {
                   (c & 7) * 2);
 }
 
+// Warp sum of n (4 or 8) per-lane values by reduce-scatter: each butterfly level
+// keeps half of the remaining rows and ships the other half (n/2 + n/4 + ... + the
+// last log2(32/n) full levels: 9 shuffles for n = 8, 6 for n = 4, instead of 5n).
+// Returns the full sum of row (lane >> (5 - log2 n)) in every lane.
+template <int n>
+__device__ __forceinline__ float warp_sum_scatter(const float (&v)[kR], int lane) {
+  static_assert(n == 4 || n == 8, "rows per item");
+  float w[n];
+#pragma unroll
+  for (int i = 0; i < n; ++i) w[i] = v[i];
+  int width = n;
+#pragma unroll
+  for (int bit = 16; bit >= 1; bit >>= 1) {
+    if (width > 1) {
+      const bool hi = lane & bit;
+      const int half = width / 2;
+#pragma unroll
+      for (int i = 0; i < n / 2; ++i) {
+        if (i < half) {
+          const float mine = hi ? w[half + i] : w[i];
+          const float other = hi ? w[i] : w[half + i];
+          w[i] = mine + __shfl_xor_sync(0xffffffffu, other, bit);
+        }
+      }
+      width = half;
+    } else {
+      w[0] += __shfl_xor_sync(0xffffffffu, w[0], bit);
+    }
+  }
+  return w[0];
+}
+
 template <typename ItemT>
 __device__ __forceinline__ void item_blocks(const KParams& p, const ItemT& it, int& nbA, int& nb,
                                             int64_t& pbase, int64_t& dbase) {
@@ -215,8 +247,8 @@ struct NoFast {
                          const float (&)[kR], const Other&) const {}
 };
 
-template <typename T, bool kCausal = false, typename LoadItem, typename Finish, typename MergeUnit,
-          typename Fast = NoFast>
+template <typename T, bool kCausal = false, int kRows = kR, typename LoadItem, typename Finish,
+          typename MergeUnit, typename Fast = NoFast>
 __device__ void run(const KParams& p, uint8_t* smem_raw, Shared* sh, uint32_t tmem, int pi,
                     LoadItem&& load_item_at, Finish&& finish, MergeUnit&& merge_unit,
                     const Fast& fast = Fast()) {
@@ -455,6 +487,7 @@ __device__ void run(const KParams& p, uint8_t* smem_raw, Shared* sh, uint32_t tm
       if (t == 0) dbg(p, 26, g);
       // rows >= R keep m = 0 and x = -inf: their exps are exactly 0, no NaN, and
       // every row's arithmetic stays branch-free (the rows interleave for ILP).
+      // kRows (4 or 8, per launch) bounds the rows any VEC item of the plan has
       float m[kR], lp[kR];
 #pragma unroll
       for (int r = 0; r < kR; ++r) { m[r] = r < R ? -INFINITY : 0.f; lp[r] = 0.f; }
@@ -490,37 +523,46 @@ __device__ void run(const KParams& p, uint8_t* smem_raw, Shared* sh, uint32_t tm
         float x[kR], v[kR];
         const int key = (j < nbA ? it.pk0 + j * kBK : it.dk0 + (j - nbA) * kBK) + t;
 #pragma unroll
-        for (int r = 0; r < kR; ++r) {
+        for (int r = 0; r < kRows; ++r) {
           const bool vis = !causal || key <= (j < nbA ? limp[r] : limd[r]);
           x[r] = (valid && r < R && vis) ? __uint_as_float(sr[r]) * sc : -INFINITY;
           v[r] = x[r];
         }
 #pragma unroll
-        for (int r = 0; r < kR; ++r) v[r] = dev::warp_max_f32(v[r]);  // one CREDUX.MAX.F32 per row
+        for (int r = 0; r < kRows; ++r) v[r] = dev::warp_max_f32(v[r]);  // one CREDUX.MAX.F32 per row
         if (lane == 0) {
 #pragma unroll
-          for (int r = 0; r < kR; ++r) sh->red[g & 1][warp][r] = v[r];
+          for (int r = 0; r < kRows; ++r) sh->red[g & 1][warp][r] = v[r];
         }
         if (t == 0) dbg(p, 11, g);
         named_sync_softmax(pi);  // red[g & 1] is rewritten two blocks later, after another barrier
 
         if (t == 0) dbg(p, 12, g);
         const float (&rd)[4][kR] = sh->red[g & 1];
-        float alpha[kR];
-        bool any_rescale = false;
+        // the running maxima are identical in every thread, so `any_up` is CTA-uniform
+        // and the rescale exponentials run only on blocks that raise a row's maximum
+        float alpha[kR], bmax[kR];
+        bool any_up = false, any_rescale = false;
 #pragma unroll
-        for (int r = 0; r < kR; ++r) {
-          const float bm = fmaxf(fmaxf(rd[0][r], rd[1][r]), fmaxf(rd[2][r], rd[3][r]));
-          const bool up = bm > m[r] + kRescaleThreshold;  // also the first block (m = -inf)
-          alpha[r] = up ? dev::ex2(m[r] - bm) : 1.f;
-          any_rescale |= up && (m[r] != -INFINITY);
-          m[r] = up ? bm : m[r];
+        for (int r = 0; r < kRows; ++r) {
+          bmax[r] = fmaxf(fmaxf(rd[0][r], rd[1][r]), fmaxf(rd[2][r], rd[3][r]));
+          alpha[r] = 1.f;
+          any_up |= bmax[r] > m[r] + kRescaleThreshold;  // also the first block (m = -inf)
+        }
+        if (any_up) {
+#pragma unroll
+          for (int r = 0; r < kRows; ++r) {
+            const bool up = bmax[r] > m[r] + kRescaleThreshold;
+            alpha[r] = up ? dev::ex2(m[r] - bmax[r]) : 1.f;
+            any_rescale |= up && (m[r] != -INFINITY);
+            m[r] = up ? bmax[r] : m[r];
+          }
         }
         float e[kR];
 #pragma unroll
-        for (int r = 0; r < kR; ++r) {
+        for (int r = 0; r < kRows; ++r) {
           e[r] = dev::ex2(x[r] - (m[r] == -INFINITY ? 0.f : m[r]));  // all-masked rows: 0
-          lp[r] = lp[r] * alpha[r] + e[r];
+          lp[r] = any_up ? lp[r] * alpha[r] + e[r] : lp[r] + e[r];
         }
         // P^T (single buffer): PV_{g-1} must be done reading it (and O before rescale);
         // it was issued a whole softmax ago, so this wait rarely blocks.
@@ -531,7 +573,7 @@ __device__ void run(const KParams& p, uint8_t* smem_raw, Shared* sh, uint32_t tm
         }
         if (t == 0) dbg(p, 14, g);
 #pragma unroll
-        for (int r = 0; r < kR; ++r) {
+        for (int r = 0; r < kRows; ++r) {
           if (r < R) {
             T h;
             if constexpr (sizeof(T) == 2) h = T(e[r]);
@@ -545,7 +587,7 @@ __device__ void run(const KParams& p, uint8_t* smem_raw, Shared* sh, uint32_t tm
           dev::tmem_ld16(tO, o);
           dev::tmem_wait_ld();
 #pragma unroll
-          for (int r = 0; r < kR; ++r) o[r] = __float_as_uint(__uint_as_float(o[r]) * alpha[r]);
+          for (int r = 0; r < kRows; ++r) o[r] = __float_as_uint(__uint_as_float(o[r]) * alpha[r]);
           dev::tmem_st16(tO, o);
           dev::tmem_wait_st();
         }
@@ -559,17 +601,10 @@ __device__ void run(const KParams& p, uint8_t* smem_raw, Shared* sh, uint32_t tm
       }
       // ---- item end: l per row, then O^T lane t = value column t
       {
-        float v[kR];
-#pragma unroll
-        for (int r = 0; r < kR; ++r) v[r] = lp[r];
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1)
-#pragma unroll
-          for (int r = 0; r < kR; ++r) v[r] += __shfl_xor_sync(0xffffffffu, v[r], o);
-        if (lane == 0) {
-#pragma unroll
-          for (int r = 0; r < kR; ++r) sh->red[g & 1][warp][r] = v[r];
-        }
+        // lane l holds the warp sum of row l >> (5 - log2 kRows)
+        constexpr int kLaneShift = kRows == 8 ? 2 : 3;
+        const float s = warp_sum_scatter<kRows>(lp, lane);
+        if ((lane & ((1 << kLaneShift) - 1)) == 0) sh->red[g & 1][warp][lane >> kLaneShift] = s;
       }
       named_sync_softmax(pi);
       float L[kR];
@@ -577,7 +612,7 @@ __device__ void run(const KParams& p, uint8_t* smem_raw, Shared* sh, uint32_t tm
         const float (&rd)[4][kR] = sh->red[g & 1];
 #pragma unroll
         for (int r = 0; r < kR; ++r)
-          L[r] = r < R ? (rd[0][r] + rd[1][r]) + (rd[2][r] + rd[3][r]) : 0.f;
+          L[r] = (r < kRows && r < R) ? (rd[0][r] + rd[1][r]) + (rd[2][r] + rd[3][r]) : 0.f;
       }
       if (t == 0) dbg(p, 7, g - 1);
       dev::mbar_wait(&sh->o_full[b], (k >> 1) & 1);

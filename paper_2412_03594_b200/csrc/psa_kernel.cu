@@ -1035,7 +1035,7 @@ __device__ __forceinline__ void setmaxnreg_dec_88() { asm volatile("setmaxnreg.d
 __device__ __forceinline__ void setmaxnreg_dec_128() { asm volatile("setmaxnreg.dec.sync.aligned.u32 128;"); }
 __device__ __forceinline__ void setmaxnreg_inc_128() { asm volatile("setmaxnreg.inc.sync.aligned.u32 128;"); }
 
-template <typename T, int kEmu, bool kCausal>
+template <typename T, int kEmu, bool kCausal, int kRows>
 __global__ void __launch_bounds__(kV2Threads, 1) psa_v2(const __grid_constant__ KParams p) {
   extern __shared__ __align__(1024) uint8_t smem[];
   __shared__ tile2::Shared s_t2;
@@ -1138,7 +1138,7 @@ __global__ void __launch_bounds__(kV2Threads, 1) psa_v2(const __grid_constant__ 
                       const float (&L)[dec::kR], const float (&ov)[dec::kR]) {
       dec_finish<T>(p, &s_dec[pi], it, oidx, idx, t, R, m, L, ov, pi);
     };
-    dec::run<T, kCausal>(p, smem + pi * half, &s_dec[pi], tmem + 64u * uint32_t(pi), pi, load_at, finish,
+    dec::run<T, kCausal, kRows>(p, smem + pi * half, &s_dec[pi], tmem + 64u * uint32_t(pi), pi, load_at, finish,
                 arrive_dec, DecFast<T>{p});
     // diagnostics: decode-phase record at trace row num_items + 3072 + CTA:
     // {softmax warps, producer, MMA warp, merge warps} done
@@ -1285,7 +1285,11 @@ int launch_v2(const KParams& p_in, int32_t num_sms, void* stream) {
   if (p.use_dec) {
     smem = std::max(smem, size_t(p.dec_pipes) * dec::pipe_stride(p.dec_slots));
   }
-  auto kern = (p.flags & PSA_FLAG_CAUSAL) ? psa_v2<T, kV2EmuEvery, true> : psa_v2<T, kV2EmuEvery, false>;
+  // decode rows per item: 4 (one token of gqa <= 4 heads) or 8
+  const bool r4 = p.max_vec_rows <= 4;
+  auto kern = (p.flags & PSA_FLAG_CAUSAL)
+                  ? (r4 ? psa_v2<T, kV2EmuEvery, true, 4> : psa_v2<T, kV2EmuEvery, true, 8>)
+                  : (r4 ? psa_v2<T, kV2EmuEvery, false, 4> : psa_v2<T, kV2EmuEvery, false, 8>);
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        int(smem));
   if (e != cudaSuccess) return e;

@@ -353,6 +353,9 @@ std::string build_plan(const PlanInput& in, const PlanOptions& opt, Plan* out) {
   out->num_units = int32_t(units.size());
   out->workspace_rows = ws;
   out->tile_ctas = out->num_tile_items > 0 ? int32_t(ctas) : 0;
+  out->max_vec_rows = 0;
+  for (const auto& it : items)
+    if (it[kItKind] == kItemVec) out->max_vec_rows = std::max(out->max_vec_rows, it[kItRows]);
   return "";
 }
 

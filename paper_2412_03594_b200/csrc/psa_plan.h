@@ -72,6 +72,7 @@ struct Plan {
   int32_t chunk_keys = 0;
   int64_t tile_cost = 0, total_cost = 0;  // LPT cost model totals (host heuristics only)
   int32_t tile_ctas = 0;  // v2: CTAs that start on the TILE queue (the rest on decode)
+  int32_t max_vec_rows = 0;  // rows of the largest VEC item
 };
 
 // Returns "" on success, else the validation message (maps to PSA_INVALID_ARGUMENT).

@@ -61,6 +61,7 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--config", default="c2")
     ap.add_argument("--ctas-per-sm", type=int, default=0)
+    ap.add_argument("--num-sms", type=int, default=0)
     ap.add_argument("--min-chunk", type=int, default=0)
     ap.add_argument("--waves", type=int, default=0)
     ap.add_argument("--groups", type=int, default=0)
@@ -76,7 +77,7 @@ def main():
     b = W.make_batch(spec, dev)
     op = P.PrefixSharedAttention(b["cu_req"], b["cu_q"], b["cu_prefix"], b["cu_distinct"],
                                  spec.Hq, spec.Hkv, spec.d, spec.dv, spec.torch_dtype, dev,
-                                 options=P.PlanOptions(ctas_per_sm=args.ctas_per_sm,
+                                 options=P.PlanOptions(ctas_per_sm=args.ctas_per_sm, num_sms=args.num_sms,
                                                        min_chunk_keys=args.min_chunk,
                                                        target_waves=args.waves))
     inputs = (b["q"], b["k_prefix"], b["v_prefix"], b["k_distinct"], b["v_distinct"])
