@@ -55,6 +55,38 @@ __device__ __forceinline__ bool mbar_test(uint64_t* bar, uint32_t parity) {
   return ok != 0;
 }
 // Blocks until the phase with the given parity has completed.
+#ifdef PSA_BOUNDED_WAIT
+// Debug build (build.py with PSA_DEBUG_BUILD=1 -> libpsa_debug.so): a wait that has
+// not completed after ~2^31 polls (seconds) records who hung on which barrier in
+// psa_hang_info and traps, instead of spinning until the host's timeout.
+__device__ int psa_hang_info[8];
+__device__ __noinline__ void mbar_hang(uint64_t* bar, uint32_t parity) {
+  if (atomicCAS(&psa_hang_info[0], 0, 1) == 0) {
+    psa_hang_info[1] = int(blockIdx.x);
+    psa_hang_info[2] = int(threadIdx.x);
+    psa_hang_info[3] = int(smem_u32(bar));
+    psa_hang_info[4] = int(parity);
+    __threadfence_system();
+    printf("psa: mbarrier wait hung: block %d thread %d barrier smem+0x%x parity %u\n",
+           int(blockIdx.x), int(threadIdx.x), smem_u32(bar), parity);
+  }
+  __trap();
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  uint32_t ok = 0;
+  for (uint32_t n = 0; n < (1u << 31); ++n) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(ok)
+        : "r"(smem_u32(bar)), "r"(parity)
+        : "memory");
+    if (ok) return;
+  }
+  mbar_hang(bar, parity);
+}
+#else
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   asm volatile(
       "{\n\t.reg .pred p;\n\t"
@@ -64,6 +96,7 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
       "r"(parity)
       : "memory");
 }
+#endif
 
 // ---- TMA -----------------------------------------------------------------------
 __device__ __forceinline__ void tma_prefetch_desc(const CUtensorMap* m) {
@@ -281,6 +314,17 @@ struct MergeQueue {
 
 __device__ __forceinline__ int ld_vol(const int* p) { return *reinterpret_cast<const volatile int*>(p); }
 __device__ __forceinline__ void st_vol(int* p, int v) { *reinterpret_cast<volatile int*>(p) = v; }
+// The queue's sequence words are its synchronisation flags: a writer publishes an
+// entry with a release store of seq, a reader takes it with an acquire load (CTA
+// scope, shared memory), so the entry's payload is ordered without a separate fence.
+__device__ __forceinline__ int ld_acq_cta(const int* p) {
+  int v;
+  asm volatile("ld.acquire.cta.shared::cta.b32 %0, [%1];" : "=r"(v) : "r"(smem_u32(p)) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_rel_cta(int* p, int v) {
+  asm volatile("st.release.cta.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(p)), "r"(v) : "memory");
+}
 
 // One thread.
 __device__ __forceinline__ void mq_init(MergeQueue* q) {
@@ -293,10 +337,9 @@ __device__ __forceinline__ void mq_push(MergeQueue* q, int u) {
   atomicAdd(&q->outstanding, 1);
   const int t = atomicAdd(&q->resv, 1);
   const int i = t & (MergeQueue::kCap - 1);
-  while (ld_vol(&q->seq[i]) != t) __nanosleep(32);
+  while (ld_acq_cta(&q->seq[i]) != t) __nanosleep(32);  // the reader of ticket t - kCap is done
   st_vol(&q->unit[i], u);
-  __threadfence_block();
-  st_vol(&q->seq[i], t + 1);
+  st_rel_cta(&q->seq[i], t + 1);
 }
 
 // One producer (thread) is done pushing; its pushes precede this in program order
@@ -324,11 +367,10 @@ __device__ __forceinline__ void mq_drain(MergeQueue* q, int closers, Task&& task
       const int t = atomicAdd(&q->head, 1);
       const int i = t & (MergeQueue::kCap - 1);
       for (;;) {
-        if (ld_vol(&q->seq[i]) == t + 1) {
+        if (ld_acq_cta(&q->seq[i]) == t + 1) {
           u = ld_vol(&q->unit[i]);
           ok = 1;
-          __threadfence_block();
-          st_vol(&q->seq[i], t + MergeQueue::kCap);
+          st_rel_cta(&q->seq[i], t + MergeQueue::kCap);  // after the payload read
           break;
         }
         if (ld_vol(&q->closed) >= closers) {

@@ -1109,7 +1109,7 @@ __global__ void __launch_bounds__(kV2Threads, 1) psa_v2(const __grid_constant__ 
                     p.trace + (int64_t(p.num_items) + row + blockIdx.x) * 4 + field),
                 (unsigned long long)globaltimer());
   };
-  if (p.use_tiles) {
+  auto tile_phase = [&]() {
     if (warp < 8) {
       setmaxnreg_inc_168();
       tile2::run_softmax<T, kEmu, kCausal>(p, &s_t2, tmem, load_at);
@@ -1126,12 +1126,9 @@ __global__ void __launch_bounds__(kV2Threads, 1) psa_v2(const __grid_constant__ 
       }
       setmaxnreg_inc_128();
     }
-    dev::tc_fence_before();
-    __syncthreads();
-    dev::tc_fence_after();
-    if (threadIdx.x == 0) phase_mark(3);
-  }
-  if (p.use_dec && (warp >> 3) < p.dec_pipes) {
+  };
+  auto dec_phase = [&]() {
+    if ((warp >> 3) >= p.dec_pipes) return;
     const int pi = warp >> 3;
     const size_t half = dec::pipe_stride(p.dec_slots);
     auto finish = [&](const ItemRec& it, const int64_t* oidx, int idx, int t, int R, const float (&m)[dec::kR],
@@ -1144,6 +1141,35 @@ __global__ void __launch_bounds__(kV2Threads, 1) psa_v2(const __grid_constant__ 
     // {softmax warps, producer, MMA warp, merge warps} done
     const int rw = (warp & 7) < 4 ? 0 : (warp & 7) == 4 ? 1 : (warp & 7) == 5 ? 2 : 3;
     phase_mark(rw, 3072);
+  };
+  // Between the phases: every role of the first phase is done (its TMA loads were all
+  // consumed, its TMEM reads/writes completed) before the second reuses shared memory
+  // and TMEM; generic-proxy shared-memory accesses are ordered before the next
+  // phase's TMA writes.
+  auto phase_gap = [&]() {
+    dev::fence_proxy_async_smem();
+    dev::tc_fence_before();
+    __syncthreads();
+    dev::tc_fence_after();
+    if (threadIdx.x == 0) phase_mark(3);
+  };
+  // Horizontal fusion across SMs: CTAs [0, n_tile_ctas) start on the TILE queue
+  // (tensor-bound prefix tiles), the others on the decode queue (HBM streaming), so
+  // both kinds of work run at the same time; a CTA whose queue is empty moves on
+  // to the other one (each queue is drained exactly once per CTA).
+  const bool tiles_first = int(blockIdx.x) < p.n_tile_ctas || !p.use_dec;
+  if (tiles_first) {
+    if (p.use_tiles) {
+      tile_phase();
+      phase_gap();
+    }
+    if (p.use_dec) dec_phase();
+  } else {
+    dec_phase();
+    if (p.use_tiles) {
+      phase_gap();
+      tile_phase();
+    }
   }
   __syncthreads();
   if (p.trace_cap > 0 && threadIdx.x == 0) trace_item(p, p.num_items + int(blockIdx.x), -1, t_kernel0);
