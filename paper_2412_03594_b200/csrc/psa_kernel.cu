@@ -1296,6 +1296,8 @@ int launch_v2(const KParams& p_in, int32_t num_sms, void* stream) {
   const int dbg = dbg_env ? std::atoi(dbg_env) : 0;
   p.dec_pipes = (dbg & 1) ? 1 : 2;
   p.tile_pp = (dbg & 32) ? 0 : 1;
+  p.tile_turns = 0;  // measured: no gain on c3/c5 (profiles/r2_turns_ab.txt)
+  if (const char* t = std::getenv("PSA_TILE_TURNS")) p.tile_turns = std::atoi(t);  // diagnostics: 0-3
   p.dec_fast = (dbg & 256) ? 0 : 1;
   const char* dbg_cta = std::getenv("PSA_DBG_CTA");
   p.dbg_cta = dbg_cta ? std::atoi(dbg_cta) : 0;
