@@ -1142,35 +1142,18 @@ __global__ void __launch_bounds__(kV2Threads, 1) psa_v2(const __grid_constant__ 
     const int rw = (warp & 7) < 4 ? 0 : (warp & 7) == 4 ? 1 : (warp & 7) == 5 ? 2 : 3;
     phase_mark(rw, 3072);
   };
-  // Between the phases: every role of the first phase is done (its TMA loads were all
-  // consumed, its TMEM reads/writes completed) before the second reuses shared memory
-  // and TMEM; generic-proxy shared-memory accesses are ordered before the next
-  // phase's TMA writes.
-  auto phase_gap = [&]() {
-    dev::fence_proxy_async_smem();
+  // Tile phase, then decode phase. Between them every role of the tile phase is done
+  // (its TMA loads were all consumed, its TMEM reads/writes completed) before the
+  // decode pipelines reuse shared memory and TMEM. (Each phase body is inlined once:
+  // the kernel's instruction footprint is itself a measured cost.)
+  if (p.use_tiles) {
+    tile_phase();
     dev::tc_fence_before();
     __syncthreads();
     dev::tc_fence_after();
     if (threadIdx.x == 0) phase_mark(3);
-  };
-  // Horizontal fusion across SMs: CTAs [0, n_tile_ctas) start on the TILE queue
-  // (tensor-bound prefix tiles), the others on the decode queue (HBM streaming), so
-  // both kinds of work run at the same time; a CTA whose queue is empty moves on
-  // to the other one (each queue is drained exactly once per CTA).
-  const bool tiles_first = int(blockIdx.x) < p.n_tile_ctas || !p.use_dec;
-  if (tiles_first) {
-    if (p.use_tiles) {
-      tile_phase();
-      phase_gap();
-    }
-    if (p.use_dec) dec_phase();
-  } else {
-    dec_phase();
-    if (p.use_tiles) {
-      phase_gap();
-      tile_phase();
-    }
   }
+  if (p.use_dec) dec_phase();
   __syncthreads();
   if (p.trace_cap > 0 && threadIdx.x == 0) trace_item(p, p.num_items + int(blockIdx.x), -1, t_kernel0);
   if (threadIdx.x == 0) {
@@ -1296,8 +1279,6 @@ int launch_v2(const KParams& p_in, int32_t num_sms, void* stream) {
   const int dbg = dbg_env ? std::atoi(dbg_env) : 0;
   p.dec_pipes = (dbg & 1) ? 1 : 2;
   p.tile_pp = (dbg & 32) ? 0 : 1;
-  p.tile_turns = 0;  // measured: no gain on c3/c5 (profiles/r2_turns_ab.txt)
-  if (const char* t = std::getenv("PSA_TILE_TURNS")) p.tile_turns = std::atoi(t);  // diagnostics: 0-3
   p.dec_fast = (dbg & 256) ? 0 : 1;
   const char* dbg_cta = std::getenv("PSA_DBG_CTA");
   p.dbg_cta = dbg_cta ? std::atoi(dbg_cta) : 0;

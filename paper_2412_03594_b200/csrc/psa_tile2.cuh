@@ -231,16 +231,6 @@ __device__ __forceinline__ void dbg(const KParams& p, int ev, uint32_t g) {
 __device__ __forceinline__ void named_sync(int id, int threads) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(threads) : "memory");
 }
-__device__ __forceinline__ void named_arrive(int id, int threads) {
-  asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(threads) : "memory");
-}
-// Exp-phase turns of the two softmax WGs on two-slot items (named barriers 6, 7):
-// WG i waits for its turn on barrier 6 + i and hands the turn over on 7 - i. Left
-// free-running, the two WGs drift into lockstep — both exponentiate at once, share
-// MUFU, and then both wait for the tensor core (measured: ~4.5k cycles per block
-// pair for ~2k of MMA work). Taking turns keeps one slot's MMAs under the other
-// slot's softmax.
-constexpr int kTurnBar = 6;
 
 // ---------------------------------------------------------------------------
 // The tile phase. Returns when the TILE queue is drained and every role is done.
@@ -454,8 +444,6 @@ __device__ void run_softmax(const KParams& p, Shared* sh, uint32_t tmem, LoadIte
     // s_full[b] phases consumed as seen by this WG (the other WG / mode consumes some
     // of buffer 1's), and pv_done phases of single-slot items before the current one
     uint32_t hs[2] = {0u, 0u}, npv = 0;
-    const bool turns = p.tile_turns != 0;
-    if (turns && i == 1) named_arrive(kTurnBar, 256);  // WG0 takes the first turn
     for (uint32_t k = 0;; ++k) {
       const uint32_t q = k & 1;
       dev::mbar_wait(&sh->item_full[q], (k >> 1) & 1);
@@ -494,13 +482,8 @@ __device__ void run_softmax(const KParams& p, Shared* sh, uint32_t tmem, LoadIte
         ++hs[b];
         if (!warp_rows) {
           // every row of this warp is past the slot's rows (small groups): keep the
-          // barrier pace (one p_full arrival per block, after this block's S; the
-          // exp-phase turn) and skip the softmax — its P rows feed only output rows
-          // that are never written
-          if (turns && two) {
-            named_sync(kTurnBar + i, 256);
-            named_arrive(kTurnBar + 1 - i, 256);
-          }
+          // barrier pace (one p_full arrival per block, after this block's S) and skip
+          // the softmax — its P rows feed only output rows that are never written
           __syncwarp();
           if (lane == 0) dev::mbar_arrive(&sh->p_full[b]);
           continue;
@@ -508,7 +491,6 @@ __device__ void run_softmax(const KParams& p, Shared* sh, uint32_t tmem, LoadIte
         const uint32_t tS = tmem + uint32_t(b) * 128 + lane_base;
         const bool ev = threadIdx.x == 0;
         if (ev) dbg(p, 0, nblk);
-        if (turns && two && p.tile_turns >= 2) named_sync(kTurnBar + i, 256);  // this WG's turn
         dev::tc_fence_after();
         uint32_t r[4][32];
         dev::tmem_ld32(tS + 0, r[0]);
@@ -554,7 +536,6 @@ __device__ void run_softmax(const KParams& p, Shared* sh, uint32_t tmem, LoadIte
         l0 *= alpha;
         l1 *= alpha;
         const float nm = m == -INFINITY ? 0.f : -m;  // a row masked so far: P = 0
-        if (turns && two && p.tile_turns == 1) named_sync(kTurnBar + i, 256);  // this WG's exp turn
         // P = 2^(s*sc - m), packed bf16 pairs into r[c][0..15]; sums in (l0, l1)
 #pragma unroll
         for (int c = 0; c < 4; ++c) {
@@ -572,7 +553,6 @@ __device__ void run_softmax(const KParams& p, Shared* sh, uint32_t tmem, LoadIte
             r[c][e] = pack2<T>(y0, y1);
           }
         }
-        if (turns && two && p.tile_turns <= 2) named_arrive(kTurnBar + 1 - i, 256);  // the other WG's turn
         if (ev) dbg(p, 3, nblk);
         // P_n -> S_i columns [0, 64)
         {
@@ -607,7 +587,6 @@ __device__ void run_softmax(const KParams& p, Shared* sh, uint32_t tmem, LoadIte
         dev::tc_fence_before();
         __syncwarp();
         if (lane == 0) dev::mbar_arrive(&sh->p_full[b]);
-        if (turns && two && p.tile_turns == 3) named_arrive(kTurnBar + 1 - i, 256);  // the other WG's turn
         if (ev) dbg(p, 4, nblk);
       }
       if (two) {

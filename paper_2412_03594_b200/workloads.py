@@ -101,8 +101,36 @@ def config(name: str) -> Spec:
     if name == "c3_chunks":
         return Spec("c3_chunks", 32, 8, 128, 128, "bf16", "normal", [0] * 64,
                     [[(512, 512)] * 2 for _ in range(64)], seed=3)
+    if name.startswith("fig9:"):
+        for n, spec in fig9_specs():
+            if n.lower() == name[5:]:
+                return spec
     raise ValueError(f"unknown config {name!r} (c1..c5, c2_prefix, c2_decode, c3_prefix, "
-                     "c3_chunks)")
+                     "c3_chunks, fig9:<shape>)")
+
+
+def fig9_specs() -> list:
+    """Kernel-comparison shapes in the style of the paper's Fig. 9:
+    P/D/k = shared-prefix length / distinct length / requests per prefix group;
+    decoding with 32 and 256 requests, and chunked prefill (7 prefill chunks of 512
+    tokens with 512 own keys, plus 256 decoding requests). Llama-3-8B heads, bf16.
+    Names: dec{R}_{P}/{D}/{k|all}, chunked7+256_{P}/256/{k}."""
+    out = []
+    for R in (32, 256):
+        for P, D in ((256, 2048), (2048, 256), (2048, 2048), (8192, 256)):
+            for k in (R, 16, 4):
+                G = R // k
+                out.append((f"dec{R}_{P}/{D}/{'all' if k == R else k}",
+                            Spec("fig9", 32, 8, 128, 128, "bf16", "normal", [P] * G,
+                                 [[(1, D)] * k for _ in range(G)], seed=9)))
+    for P, k in ((2048, 32), (2048, 263)):
+        G = 263 // k if k < 263 else 1
+        reqs = [[(1, 256)] * k for _ in range(G)]
+        for i in range(7):  # prefill chunks spread over the groups
+            reqs[i % G].append((512, 512))
+        out.append((f"chunked7+256_{P}/256/{k}",
+                    Spec("fig9", 32, 8, 128, 128, "bf16", "normal", [P] * G, reqs, seed=9)))
+    return out
 
 
 def offsets(spec: Spec) -> dict:

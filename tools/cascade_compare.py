@@ -36,27 +36,7 @@ def timeit(fn, iters=50):
     return e0.elapsed_time(e1) / iters * 1e3
 
 
-def fig9_specs():
-    """Kernel-comparison shapes in the style of the paper's Fig. 9:
-    setting P/D/k = shared-prefix length / distinct length / requests per prefix group,
-    decoding with 32 and 256 requests, and chunked prefill (7 prefill chunks of 512
-    tokens with 512 own keys, plus 256 decoding requests). Llama-3-8B heads, bf16."""
-    out = []
-    for R in (32, 256):
-        for P, D in ((256, 2048), (2048, 256), (2048, 2048), (8192, 256)):
-            for k in (R, 16, 4):
-                G = R // k
-                out.append((f"dec{R}_{P}/{D}/{'all' if k == R else k}",
-                            W.Spec("fig9", 32, 8, 128, 128, "bf16", "normal", [P] * G,
-                                   [[(1, D)] * k for _ in range(G)], seed=9)))
-    for P, k in ((2048, 32), (2048, 263)):
-        G = 263 // k if k < 263 else 1
-        reqs = [[(1, 256)] * k for _ in range(G)]
-        for i in range(7):  # prefill chunks spread over the groups
-            reqs[i % G].append((512, 512))
-        out.append((f"chunked7+256_{P}/256/{k}",
-                    W.Spec("fig9", 32, 8, 128, 128, "bf16", "normal", [P] * G, reqs, seed=9)))
-    return out
+fig9_specs = W.fig9_specs
 
 
 def main():
