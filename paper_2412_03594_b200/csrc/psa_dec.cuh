@@ -453,8 +453,6 @@ __device__ void run(const KParams& p, uint8_t* smem_raw, Shared* sh, uint32_t tm
         (void)progress;
       }
     }
-  } else if (warp >= 6) {
-    merge_loop(p, sh, merge_unit);
   } else if (warp < 4) {
     // ================= softmax + epilogue =================
     const int t = threadIdx.x - 256 * pi;
@@ -648,6 +646,12 @@ __device__ void run(const KParams& p, uint8_t* smem_raw, Shared* sh, uint32_t tm
       }
     }
   }
+  // The pipeline's queue is drained by its merge warps (6, 7) from the start; every
+  // other warp of the pipeline joins once its role is done and the queue is closed
+  // (units with a large fan-in complete late and in bursts).
+  __syncwarp();
+  if (warp < 6) dev::mq_wait_closed(&sh->mq, 1);
+  merge_loop(p, sh, merge_unit);
 }
 
 }  // namespace dec

@@ -356,6 +356,13 @@ __device__ __forceinline__ int mq_pending(const MergeQueue* q) {
   return ld_vol(&q->resv) - ld_vol(&q->head);
 }
 
+// A warp that finished another role and will help drain the queue: sleep until every
+// producer closed it, so the helper never competes for issue slots with warps that
+// are still computing (only the backlog left at the end is shared out).
+__device__ __forceinline__ void mq_wait_closed(const MergeQueue* q, int closers) {
+  while (ld_vol(&q->closed) < closers) __nanosleep(2048);
+}
+
 // Merge warp: pop tasks until `closers` producers closed the queue and no task is
 // outstanding.
 template <typename Task>

@@ -1032,7 +1032,6 @@ constexpr int kV2EmuEvery = 4;  // every 4th exp pair of the tile softmax on the
 
 __device__ __forceinline__ void setmaxnreg_inc_168() { asm volatile("setmaxnreg.inc.sync.aligned.u32 168;"); }
 __device__ __forceinline__ void setmaxnreg_dec_88() { asm volatile("setmaxnreg.dec.sync.aligned.u32 88;"); }
-__device__ __forceinline__ void setmaxnreg_dec_128() { asm volatile("setmaxnreg.dec.sync.aligned.u32 128;"); }
 __device__ __forceinline__ void setmaxnreg_inc_128() { asm volatile("setmaxnreg.inc.sync.aligned.u32 128;"); }
 
 template <typename T, int kEmu, bool kCausal, int kRows>
@@ -1114,18 +1113,23 @@ __global__ void __launch_bounds__(kV2Threads, 1) psa_v2(const __grid_constant__ 
       setmaxnreg_inc_168();
       tile2::run_softmax<T, kEmu, kCausal>(p, &s_t2, tmem, load_at);
       phase_mark(0);
-      setmaxnreg_dec_128();
+      setmaxnreg_dec_88();
     } else {
       setmaxnreg_dec_88();
-      if (warp >= tile2::kMergeWarp0) {
-        dev::mq_drain(&s_t2.mq, 2, tile_task);
-        phase_mark(2);
-      } else {
+      if (warp < tile2::kMergeWarp0) {
         tile2::run_support<T>(p, smem, &s_t2, tmem, load_at);
         phase_mark(1);
       }
-      setmaxnreg_inc_128();
     }
+    // Merge workers: warps 10-15 from the start; every other warp joins once its tile
+    // role is done and both softmax WGs closed the queue — a tile slot can complete
+    // dozens of merge units at once (a long prefix split into many chunks: fan-in
+    // ~17), which six warps of one CTA would otherwise work off alone.
+    __syncwarp();
+    if (warp < tile2::kMergeWarp0) dev::mq_wait_closed(&s_t2.mq, 2);
+    dev::mq_drain(&s_t2.mq, 2, tile_task);
+    phase_mark(2);
+    setmaxnreg_inc_128();
   };
   auto dec_phase = [&]() {
     if ((warp >> 3) >= p.dec_pipes) return;
