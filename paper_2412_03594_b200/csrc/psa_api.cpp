@@ -344,6 +344,10 @@ psa_status psa_run(const psa_problem* prob, const psa_plan* pl, void* ws, size_t
       nt = std::max(0, std::min(grid, std::atoi(e)));
     k.n_tile_ctas = nt;
   }
+  {  // diagnostics (PSA_DEBUG bit 1024): full forward boxes for partial last blocks
+    const char* dbg = std::getenv("PSA_DEBUG");
+    k.tail_shift = (dbg && (std::atoi(dbg) & 1024)) ? 0 : 1;
+  }
   k.Hq = in.Hq; k.Hkv = in.Hkv; k.gqa = in.Hq / in.Hkv; k.d = in.d; k.dv = in.dv;
   k.max_vec_rows = pl->plan.max_vec_rows;
   k.gqa_shift = -1;

@@ -28,12 +28,24 @@ namespace psa {
 // a segment: the packed layout (one box per chunk at cache row base + key) or a
 // paged cache (one box per page; page p of the segment is table[base + p]; pages at
 // or past key_end load the all-out-of-bounds row, i.e. zeros). Issued by one lane.
+// Packed partial last block: when the item's key range [key_begin, key_end) holds a
+// full block before it, the box is shifted back by kv_shift() keys so it ends at
+// key_end — the extra rows are the previous block's (just read: L2 hits) instead of
+// the next segment's (DRAM reads that were ~0.6 GB per c4 launch). Consumers mask
+// columns [0, shift) of such a block. Used by the decode pipelines (ragged per-request
+// KV); the tile producer passes key_begin = key (forward boxes: prefix chunks are
+// long, their partial blocks rare).
+__device__ __forceinline__ int kv_shift(const KParams& p, int key, int key_end, int key_begin, int rows) {
+  return (p.tail_shift && p.page_size == 0 && key_end - key < rows && key_end - key_begin >= rows)
+             ? rows - (key_end - key) : 0;
+}
 __device__ __forceinline__ void load_kv_block(const KParams& p, uint8_t* dst, const CUtensorMap* m,
                                               uint64_t* bar, int h, bool prefix, int64_t base,
-                                              int key, int key_end, int rows) {
+                                              int key, int key_end, int key_begin, int rows) {
   if (p.page_size == 0) {
-    dev::tma_load_3d(dst, m, bar, 0, h, int(base + key));
-    dev::tma_load_3d(dst + rows * 128, m, bar, 64, h, int(base + key));
+    const int k0 = key - kv_shift(p, key, key_end, key_begin, rows);
+    dev::tma_load_3d(dst, m, bar, 0, h, int(base + k0));
+    dev::tma_load_3d(dst + rows * 128, m, bar, 64, h, int(base + k0));
     return;
   }
   const int ps = p.page_size;
@@ -346,7 +358,7 @@ __device__ void run(const KParams& p, uint8_t* smem_raw, Shared* sh, uint32_t tm
             dbg(p, w, c >> 1);
             dev::mbar_arrive_expect_tx(&sh->slot_full[s], kSlotBytes);
             load_kv_block(p, G.slot(s), w == 0 ? km : vm, &sh->slot_full[s], it.h, pre,
-                          pre ? gbase : rbase, key, end, kBK);
+                          pre ? gbase : rbase, key, end, pre ? it.pk0 : it.dk0, kBK);
           }
         }
       }
@@ -516,10 +528,13 @@ __device__ void run(const KParams& p, uint8_t* smem_raw, Shared* sh, uint32_t tm
         dev::tc_fence_before();
         __syncwarp();
         if (lane == 0) dev::mbar_arrive(&sh->s_free);
-        const bool valid = t < nvalid;
+        // a shifted partial block holds its nvalid keys in columns [shift, kBK)
+        const int shift = j < nbA ? kv_shift(p, it.pk0 + j * kBK, it.pk1, it.pk0, kBK)
+                                  : kv_shift(p, it.dk0 + (j - nbA) * kBK, it.dk1, it.dk0, kBK);
+        const bool valid = shift ? t >= shift : t < nvalid;
         // block max per row: warp reduce, then across the 4 softmax warps
         float x[kR], v[kR];
-        const int key = (j < nbA ? it.pk0 + j * kBK : it.dk0 + (j - nbA) * kBK) + t;
+        const int key = (j < nbA ? it.pk0 + j * kBK : it.dk0 + (j - nbA) * kBK) + t - shift;
 #pragma unroll
         for (int r = 0; r < kRows; ++r) {
           const bool vis = !causal || key <= (j < nbA ? limp[r] : limd[r]);

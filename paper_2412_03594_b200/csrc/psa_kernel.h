@@ -75,6 +75,7 @@ struct KParams {
   int32_t dec_pipes;    // v2: decode pipelines per CTA (2; 1 under PSA_DEBUG bit 0)
   int32_t dec_q_tma;    // tmd_q is valid (gqa is a power of two <= 16)
   int32_t tile_pp;      // v2 single-slot tile items ping-pong S buffers (0 under PSA_DEBUG bit 5)
+  int32_t tail_shift;   // packed partial last blocks read back-shifted boxes (0 under PSA_DEBUG bit 10)
   int32_t dec_fast;     // v2 decode items may merge a finished prefix partial in registers (0 under PSA_DEBUG bit 8)
   int32_t dbg_cta;      // diagnostics: CTA whose per-block events are traced (PSA_DBG_CTA, default 0)
   const int32_t* tok_lim;        // causal: per token {last prefix key, last distinct key}

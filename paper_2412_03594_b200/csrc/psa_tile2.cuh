@@ -292,7 +292,7 @@ __device__ void run_support(const KParams& p, uint8_t* smem_raw, Shared* sh, uin
             dev::mbar_arrive_expect_tx(&sh->ring_full[s], kSlotBytes);
             dbg(p, 7 + w, c >> 1);
             load_kv_block(p, G.slot(s), w == 0 ? b.km : b.vm, &sh->ring_full[s], it.h, b.prefix,
-                          b.base, b.key, b.end, kBN);
+                          b.base, b.key, b.end, b.key, kBN);  // tiles: forward boxes (no shift)
           }
         }
       }

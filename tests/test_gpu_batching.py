@@ -3,7 +3,8 @@
 for every batch — decode, distinct-chunk and prefix-chunk entries, 16-token
 blocks from the reference's KVAllocator — the paged kernel output must match
 the float64 oracle on K/V gathered through the same page tables, and be
-bit-identical to the packed kernel on the gathered tensors."""
+bit-identical to the packed kernel on the gathered tensors (packed with full forward
+boxes for partial last blocks, conftest no_tail_shift)."""
 
 import os
 
@@ -15,6 +16,7 @@ from oracle import segmented as S
 from paper_2412_03594_b200 import batching as B
 from paper_2412_03594_b200 import packed as P
 from paper_2412_03594_b200 import paged as PG
+from conftest import no_tail_shift
 
 pytestmark = pytest.mark.gpu
 FIX = np.load(os.path.join(os.path.dirname(__file__), "golden", "token_batches.npz"))
@@ -38,8 +40,9 @@ def test_token_batch_paged_launch(i):
     dr = torch.as_tensor(PG.physical_rows(np.diff(kb.cu_distinct), kb.distinct_pages, bs),
                          device="cuda")
     kp, vp, kd, vd = k_cache[pr], v_cache[pr], k_cache[dr], v_cache[dr]
-    packed = P.prefix_shared_attention_packed(q, kp, vp, kd, vd, kb.cu_req, kb.cu_q, kb.cu_prefix,
-                                              kb.cu_distinct, HKV)
+    with no_tail_shift():
+        packed = P.prefix_shared_attention_packed(q, kp, vp, kd, vd, kb.cu_req, kb.cu_q,
+                                                  kb.cu_prefix, kb.cu_distinct, HKV)
     torch.cuda.synchronize()
     assert torch.equal(out, packed)
     h = {k: t.double().cpu().numpy() for k, t in dict(q=q, kp=kp, vp=vp, kd=kd, vd=vd).items()}

@@ -1,8 +1,10 @@
 """Paged KV mode (include/psa.h page_size > 0): the kernel reads K/V through page
 tables from caches whose unused rows hold large finite garbage. The output must be
 bit-identical to the packed layout on the same data (same work items, same
-arithmetic), for every page size, with decode + prefill-chunk requests and
-segment lengths that are not page multiples."""
+arithmetic; packed with full forward boxes for partial last blocks, conftest
+no_tail_shift), for every page size, with decode + prefill-chunk requests and
+segment lengths that are not page multiples — and equal within bf16 rounding to
+the default packed launch (back-shifted partial blocks)."""
 
 import numpy as np
 import pytest
@@ -12,6 +14,7 @@ from paper_2412_03594_b200 import packed as P
 from paper_2412_03594_b200 import paged as PG
 from paper_2412_03594_b200 import workloads as W
 from paper_2412_03594_b200.errors import ValidationError
+from conftest import no_tail_shift
 
 pytestmark = pytest.mark.gpu
 
@@ -44,8 +47,13 @@ def test_paged_matches_packed_bitwise(ps):
     off = W.offsets(spec)
     args = (off["cu_req"], off["cu_q"], off["cu_prefix"], off["cu_distinct"], spec.Hq, spec.Hkv,
             spec.d, spec.dv, torch.bfloat16, "cuda")
-    ref = P.PrefixSharedAttention(*args)(b["q"], b["k_prefix"], b["v_prefix"], b["k_distinct"],
-                                         b["v_distinct"])
+    shifted = P.PrefixSharedAttention(*args)(b["q"], b["k_prefix"], b["v_prefix"], b["k_distinct"],
+                                             b["v_distinct"])
+    with no_tail_shift():
+        ref = P.PrefixSharedAttention(*args)(b["q"], b["k_prefix"], b["v_prefix"],
+                                             b["k_distinct"], b["v_distinct"])
+    torch.cuda.synchronize()
+    assert float((shifted.float() - ref.float()).abs().max()) <= 1e-2
     rng = np.random.default_rng(ps)
     pg = _paged_inputs(b, off, ps, rng)
     op = P.PrefixSharedAttention(*args, page_size=ps)
@@ -64,8 +72,9 @@ def test_paged_skewed_batch_matches_packed():
     off = W.offsets(spec)
     args = (off["cu_req"], off["cu_q"], off["cu_prefix"], off["cu_distinct"], spec.Hq, spec.Hkv,
             spec.d, spec.dv, torch.bfloat16, "cuda")
-    ref = P.PrefixSharedAttention(*args)(b["q"], b["k_prefix"], b["v_prefix"], b["k_distinct"],
-                                         b["v_distinct"])
+    with no_tail_shift():
+        ref = P.PrefixSharedAttention(*args)(b["q"], b["k_prefix"], b["v_prefix"],
+                                             b["k_distinct"], b["v_distinct"])
     pg = _paged_inputs(b, off, 16, np.random.default_rng(7))
     got = P.PrefixSharedAttention(*args, page_size=16)(
         b["q"], pg["k_prefix"], pg["v_prefix"], pg["k_distinct"], pg["v_distinct"],
