@@ -486,11 +486,13 @@ def main():
     barrier(world)
     torch.cuda.synchronize()
     with sampler:
+        torch.cuda.nvtx.range_push("timed")  # ncu --nvtx --nvtx-include "timed/": the launch list
         start.record(stream)
         for _ in range(args.steps):
             step()
         end.record(stream)
         torch.cuda.synchronize()
+        torch.cuda.nvtx.range_pop()
     barrier(world)
     ms_rank = start.elapsed_time(end) / args.steps
     ms = max_over_ranks(ms_rank, world)
