@@ -261,13 +261,21 @@ def build_plan(G, R, Hq, Hkv, d, dv, dtype, cu_req, cu_q, cu_prefix, cu_distinct
         else:
             cost.append(max(nbytes * BYTE_WEIGHT,
                             2 * _rup(it[IT_ROWS], 4) * keys * width * VEC_FLOP_WEIGHT))
-    # TILE items first (CTA-level queue), then VEC items; each by cost descending.
-    # Equal-cost VEC items: the kv heads of one (request, key chunk) side by side
-    # (psa_plan.cpp build_plan step 4).
+    # TILE items first (CTA-level queue), then VEC items. TILE items by (group, kv head)
+    # bundle: bundle cost descending, then bundle, then item cost descending; VEC items
+    # by cost descending, equal-cost VEC items with the kv heads of one (request, key
+    # chunk) side by side (psa_plan.cpp build_plan step 4).
+    bundle = {}
+    for i, it in enumerate(items):
+        if it[IT_KIND] == KIND_TILE:
+            k = it[IT_GROUP] * Hkv + it[IT_HEAD]
+            bundle[k] = bundle.get(k, 0) + cost[i]
+
     def _key(i):
         it = items[i]
         if it[IT_KIND] == KIND_TILE:
-            return (False, -cost[i], ())
+            k = it[IT_GROUP] * Hkv + it[IT_HEAD]
+            return (False, -bundle[k], (k, -cost[i]))
         return (True, -cost[i], (it[IT_GROUP], it[IT_REQUEST], it[IT_ROW0], it[IT_PK0],
                                  it[IT_DK0], it[IT_HEAD]))
     order = sorted(range(len(items)), key=_key)

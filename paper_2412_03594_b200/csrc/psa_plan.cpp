@@ -317,14 +317,28 @@ std::string build_plan(const PlanInput& in, const PlanOptions& opt, Plan* out) {
     }
   }
   // Queue order: TILE items first (CTA-level queue), then VEC items (warp-level
-  // queue); each by cost descending.
+  // queue). TILE items go by (group, kv head) bundle — all tiles that read one
+  // group's prefix for one head, in bundle-cost order (LPT over bundles), each
+  // bundle's items by cost — so a group's prefix is streamed by tiles running at the
+  // same time and re-read from L2, not DRAM (c3: a group's decode-row prefix tile no
+  // longer waits behind every prefill tile of the batch). VEC items by cost.
+  std::vector<int64_t> bundle(int64_t(in.G) * in.Hkv, 0);
+  for (size_t i = 0; i < items.size(); ++i)
+    if (items[i][kItKind] == kItemTile)
+      bundle[int64_t(items[i][kItGroup]) * in.Hkv + items[i][kItHead]] += cost[i];
   std::vector<int32_t> order(items.size());
   std::iota(order.begin(), order.end(), 0);
   std::stable_sort(order.begin(), order.end(), [&](int32_t a, int32_t b) {
     const bool ta = items[a][kItKind] == kItemTile, tb = items[b][kItKind] == kItemTile;
     if (ta != tb) return ta;
+    if (ta) {
+      const int64_t ka = int64_t(items[a][kItGroup]) * in.Hkv + items[a][kItHead];
+      const int64_t kb = int64_t(items[b][kItGroup]) * in.Hkv + items[b][kItHead];
+      if (bundle[ka] != bundle[kb]) return bundle[ka] > bundle[kb];
+      if (ka != kb) return ka < kb;
+      return cost[a] > cost[b];
+    }
     if (cost[a] != cost[b]) return cost[a] > cost[b];
-    if (ta) return false;
     // equal-cost VEC items: the kv heads of one (request, key chunk) side by side, so
     // the pipelines running at the same time read whole token rows of the cache
     const auto& x = items[a];
