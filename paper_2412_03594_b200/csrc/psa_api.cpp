@@ -350,6 +350,7 @@ psa_status psa_run(const psa_problem* prob, const psa_plan* pl, void* ws, size_t
   }
   k.Hq = in.Hq; k.Hkv = in.Hkv; k.gqa = in.Hq / in.Hkv; k.d = in.d; k.dv = in.dv;
   k.max_vec_rows = pl->plan.max_vec_rows;
+  k.dec_help = pl->plan.vec_fan_in > 2 ? 1 : 0;  // two: the in-register pair merge covers it
   k.gqa_shift = -1;
   for (int sh = 0; sh < 31; ++sh)
     if ((1 << sh) == k.gqa) k.gqa_shift = sh;

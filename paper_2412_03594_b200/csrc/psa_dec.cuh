@@ -665,7 +665,10 @@ __device__ void run(const KParams& p, uint8_t* smem_raw, Shared* sh, uint32_t tm
   // other warp of the pipeline joins once its role is done and the queue is closed
   // (units with a large fan-in complete late and in bursts).
   __syncwarp();
-  if (warp < 6) dev::mq_wait_closed(&sh->mq, 1);
+  if (warp < 6) {
+    if (!p.dec_help) return;  // units of <= 2 contributions: the merge warps suffice
+    dev::mq_wait_closed(&sh->mq, 1);
+  }
   merge_loop(p, sh, merge_unit);
 }
 

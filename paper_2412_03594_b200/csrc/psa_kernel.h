@@ -64,6 +64,7 @@ struct KParams {
   int32_t Hq, Hkv, gqa, d, dv;
   int32_t gqa_shift;     // log2(gqa) when gqa is a power of two, else -1
   int32_t max_vec_rows;  // largest VEC item of the plan (rows)
+  int32_t dec_help;      // decode merge queues get helper warps (plan has VEC units with > 2 contributions)
   uint32_t flags;
   int32_t use_tiles;     // the plan has TILE items: allocate TMEM, init barriers
   int32_t use_vec_fast;  // bf16/f16, d == dv in {64, 128}: TMA-staged decode path

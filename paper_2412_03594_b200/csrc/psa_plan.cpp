@@ -368,8 +368,13 @@ std::string build_plan(const PlanInput& in, const PlanOptions& opt, Plan* out) {
   out->workspace_rows = ws;
   out->tile_ctas = out->num_tile_items > 0 ? int32_t(ctas) : 0;
   out->max_vec_rows = 0;
-  for (const auto& it : items)
-    if (it[kItKind] == kItemVec) out->max_vec_rows = std::max(out->max_vec_rows, it[kItRows]);
+  out->vec_fan_in = 0;
+  for (const auto& it : items) {
+    if (it[kItKind] != kItemVec) continue;
+    out->max_vec_rows = std::max(out->max_vec_rows, it[kItRows]);
+    for (int32_t u = it[kItUnit0]; u < it[kItUnit1]; ++u)
+      out->vec_fan_in = std::max(out->vec_fan_in, int32_t(unit_items[u].size()));
+  }
   return "";
 }
 

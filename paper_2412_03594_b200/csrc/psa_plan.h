@@ -73,6 +73,7 @@ struct Plan {
   int64_t tile_cost = 0, total_cost = 0;  // LPT cost model totals (host heuristics only)
   int32_t tile_ctas = 0;  // v2: CTAs that start on the TILE queue (the rest on decode)
   int32_t max_vec_rows = 0;  // rows of the largest VEC item
+  int32_t vec_fan_in = 0;    // most contributions of a merge unit a VEC item shares
 };
 
 // Returns "" on success, else the validation message (maps to PSA_INVALID_ARGUMENT).
