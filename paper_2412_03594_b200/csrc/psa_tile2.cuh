@@ -34,6 +34,24 @@
 
 #include "psa_device.cuh"
 
+// PSA_MMA_WARP_WIDE (default): the MMA role runs on all 32 lanes of its warp and
+// issues through elect.sync (psa_device.cuh *_w forms), so ptxas emits straight-line
+// UTCHMMA sequences instead of one elect/R2UR waterfall loop per instruction (the
+// lane-0 form spent ~85 cycles issuing each 64-cycle MMA: c3 2985 -> 2801 us, c4
+// 612 -> 600 us, c5 15.5 -> 14.6 ms). 0 = lane 0 alone (diagnostics).
+#ifndef PSA_MMA_WARP_WIDE
+#define PSA_MMA_WARP_WIDE 1
+#endif
+#if PSA_MMA_WARP_WIDE
+#define PSA_MMA_TS dev::mma_f16_ts_w
+#define PSA_MMA_SS dev::mma_f16_ss_w
+#define PSA_MMA_COMMIT dev::mma_commit_w
+#else
+#define PSA_MMA_TS dev::mma_f16_ts
+#define PSA_MMA_SS dev::mma_f16_ss
+#define PSA_MMA_COMMIT dev::mma_commit
+#endif
+
 namespace psa {
 namespace tile2 {
 
@@ -178,6 +196,31 @@ __device__ __forceinline__ void exp2_poly2(float& y0, float& y1, float x0, float
   y1 = __uint_as_float(r1);
 }
 
+// K/V ring positions of global block j. Interleaved (default): K_j = 2j, V_j = 2j + 1.
+// Split ring (PSA_TILE_SPLIT_RING=1): K_j in slots [0, NR/2), V_j in [NR/2, NR), each a
+// FIFO of its own, loaded in the MMA's consumption order, so a single-slot item's K
+// loads never wait behind a V slot held until its PV completes. Measured: c2_prefix
+// 40.2 -> 38.3 us but c2 130 -> 135 us (the earlier tile loads compete with the decode
+// CTAs for HBM), c3 / c5 unchanged; left off.
+#ifndef PSA_TILE_SPLIT_RING
+#define PSA_TILE_SPLIT_RING 0
+#endif
+constexpr bool kSplitRing = PSA_TILE_SPLIT_RING != 0;
+struct RingPos {
+  uint32_t NR, NH;
+  __device__ __forceinline__ explicit RingPos(uint32_t nr) : NR(nr), NH(nr / 2 > 0 ? nr / 2 : 1) {}
+  __device__ __forceinline__ uint32_t kslot(uint32_t j) const { return kSplitRing ? j % NH : (2 * j) % NR; }
+  __device__ __forceinline__ uint32_t vslot(uint32_t j) const {
+    return kSplitRing ? NH + j % NH : (2 * j + 1) % NR;
+  }
+  __device__ __forceinline__ uint32_t kpar(uint32_t j) const {
+    return kSplitRing ? (j / NH) & 1 : ((2 * j) / NR) & 1;
+  }
+  __device__ __forceinline__ uint32_t vpar(uint32_t j) const {
+    return kSplitRing ? (j / NH) & 1 : ((2 * j + 1) / NR) & 1;
+  }
+};
+
 struct Block {
   const CUtensorMap* km;
   const CUtensorMap* vm;
@@ -247,13 +290,13 @@ __device__ void run_support(const KParams& p, uint8_t* smem_raw, Shared* sh, uin
                             LoadItem&& load_item_at) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const Geo G = carve(smem_raw, p.tile_stages);
-  const uint32_t NR = uint32_t(p.tile_stages);
+  const RingPos R(uint32_t(p.tile_stages));
   const int gqa = p.gqa;
   const int tile_rows = gqa * (kM / gqa);
 
   if (warp == kProducerWarp) {
     // ============================ producer ============================
-    uint32_t c = 0;  // ring loads issued
+    uint32_t cb = 0;  // K/V blocks issued (global block index j = cb + item block)
     for (uint32_t k = 0;; ++k) {
       const uint32_t q = k & 1;
       dev::mbar_wait(&sh->item_empty[q], ((k >> 1) & 1) ^ 1);
@@ -284,23 +327,38 @@ __device__ void run_support(const KParams& p, uint8_t* smem_raw, Shared* sh, uin
           for (int ch = 0; ch < 2; ++ch)
             dev::tma_load_4d(G.q(i) + ch * (kM * 128), &p.tm_q, &sh->q_full, ch * 64, 0, it.h,
                              t0 + i * (kM / gqa));
-        for (int jb = 0; jb < nb; ++jb) {
+        // K_j / V_j ring loads in the order the MMA issuer consumes them (a split ring
+        // never blocks an earlier-needed load behind a later one)
+        auto load = [&](int w, int jb) {
           const Block b = block_at(p, it, jb, nbA, pbase, dbase);
-          for (int w = 0; w < 2; ++w, ++c) {  // K_jb then V_jb
-            const uint32_t s = c % NR;
-            dev::mbar_wait(&sh->ring_empty[s], ((c / NR) & 1) ^ 1);
-            dev::mbar_arrive_expect_tx(&sh->ring_full[s], kSlotBytes);
-            dbg(p, 7 + w, c >> 1);
-            load_kv_block(p, G.slot(s), w == 0 ? b.km : b.vm, &sh->ring_full[s], it.h, b.prefix,
-                          b.base, b.key, b.end, b.key, kBN);  // tiles: forward boxes (no shift)
+          const uint32_t j = cb + uint32_t(jb);
+          const uint32_t s = w == 0 ? R.kslot(j) : R.vslot(j);
+          dev::mbar_wait(&sh->ring_empty[s], (w == 0 ? R.kpar(j) : R.vpar(j)) ^ 1);
+          dev::mbar_arrive_expect_tx(&sh->ring_full[s], kSlotBytes);
+          dbg(p, 7 + w, j);
+          load_kv_block(p, G.slot(s), w == 0 ? b.km : b.vm, &sh->ring_full[s], it.h, b.prefix,
+                        b.base, b.key, b.end, b.key, kBN);  // tiles: forward boxes (no shift)
+        };
+        if (kSplitRing && !two && p.tile_pp != 0) {  // one slot: S(0), S(1), PV(0), S(2), PV(1) ...
+          load(0, 0);
+          for (int jb = 1; jb < nb; ++jb) {
+            load(0, jb);
+            load(1, jb - 1);
+          }
+          load(1, nb - 1);
+        } else {
+          for (int jb = 0; jb < nb; ++jb) {
+            load(0, jb);
+            load(1, jb);
           }
         }
+        cb += uint32_t(nb);
       }
       __syncwarp();
     }
   } else if (warp == kMmaWarp) {
     // ============================ MMA issuer ============================
-    if (lane == 0) {
+    if (PSA_MMA_WARP_WIDE || lane == 0) {
       constexpr uint32_t fmt = AbFormat<T>::v;
       const uint32_t idesc_s = dev::umma_idesc_f16(fmt, kM, kBN, 0, 0);
       const uint32_t idesc_o = dev::umma_idesc_f16(fmt, kM, kD, 0, 1);
@@ -313,7 +371,7 @@ __device__ void run_support(const KParams& p, uint8_t* smem_raw, Shared* sh, uin
         const int idx = sh->item_idx[q];
         if (idx < 0) break;
         const auto it = load_item_at(idx);
-        dev::mbar_arrive(&sh->item_empty[q]);
+        if (lane == 0) dev::mbar_arrive(&sh->item_empty[q]);
         int nbA, nb;
         int64_t pbase, dbase;
         item_shape(p, it, nbA, nb, pbase, dbase);
@@ -324,10 +382,11 @@ __device__ void run_support(const KParams& p, uint8_t* smem_raw, Shared* sh, uin
         auto issue_pv = [&](int pb, int o, uint32_t vslot, bool first) {
           const uint32_t v_addr = dev::smem_u32(G.slot(vslot));
           const uint32_t tP = tmem + uint32_t(pb) * 128, tO = tmem + kTmemO + uint32_t(o) * 128;
+          const uint64_t b0 = dev::umma_desc_sw128(v_addr, kBN * 128, 1024);
 #pragma unroll
-          for (int kk = 0; kk < kBN / 16; ++kk) {
-            const uint64_t b = dev::umma_desc_sw128(v_addr + kk * (16 * 128), kBN * 128, 1024);
-            dev::mma_f16_ts(tO, tP + kk * 8, b, idesc_o, (!first || kk > 0) ? 1u : 0u);
+          for (int kk = 0; kk < kBN / 16; ++kk) {  // descriptor start address is addr >> 4
+            const uint64_t b = b0 + uint64_t((kk * (16 * 128)) >> 4);
+            PSA_MMA_TS(tO, tP + kk * 8, b, idesc_o, (!first || kk > 0) ? 1u : 0u);
           }
         };
         // S buffer sb = Q_qi K^T
@@ -335,23 +394,25 @@ __device__ void run_support(const KParams& p, uint8_t* smem_raw, Shared* sh, uin
           const uint32_t k_addr = dev::smem_u32(G.slot(kslot));
           const uint32_t q_addr = dev::smem_u32(G.q(qi));
           const uint32_t tS = tmem + uint32_t(sb) * 128;
+          const uint64_t a0 = dev::umma_desc_sw128(q_addr, 16, 1024);
+          const uint64_t b0 = dev::umma_desc_sw128(k_addr, 16, 1024);
 #pragma unroll
           for (int kk = 0; kk < kD / 16; ++kk) {
             const uint32_t ch = kk >> 2, w = (kk & 3) * 32;
-            const uint64_t a = dev::umma_desc_sw128(q_addr + ch * (kM * 128) + w, 16, 1024);
-            const uint64_t b = dev::umma_desc_sw128(k_addr + ch * (kBN * 128) + w, 16, 1024);
-            dev::mma_f16_ss(tS, a, b, idesc_s, kk > 0 ? 1u : 0u);
+            const uint64_t a = a0 + uint64_t((ch * (kM * 128) + w) >> 4);
+            const uint64_t b = b0 + uint64_t((ch * (kBN * 128) + w) >> 4);
+            PSA_MMA_SS(tS, a, b, idesc_s, kk > 0 ? 1u : 0u);
           }
-          dev::mma_commit(&sh->s_full[sb]);
+          PSA_MMA_COMMIT(&sh->s_full[sb]);
         };
         if (ns == 2 || p.tile_pp == 0) {
           // two slots share every K/V block: per block n, slot i: PV_i(n-1) then S_i(n)
           // (S_i(n) overwrites P_i(n-1); MMAs of one thread execute in issue order)
           for (int n = 0; n < nb; ++n) {
-            const uint32_t cK = 2 * (gb + n), sK = cK % NR;
-            const uint32_t cV = cK - 1, sV = cV % NR;  // V_{n-1}
-            dev::mbar_wait(&sh->ring_full[sK], (cK / NR) & 1);
-            if (n > 0) dev::mbar_wait(&sh->ring_full[sV], (cV / NR) & 1);
+            const uint32_t jK = gb + n, sK = R.kslot(jK);
+            const uint32_t sV = R.vslot(jK - 1);  // V_{n-1}
+            dev::mbar_wait(&sh->ring_full[sK], R.kpar(jK));
+            if (n > 0) dev::mbar_wait(&sh->ring_full[sV], R.vpar(jK - 1));
             dev::tc_fence_after();
             for (int i = 0; i < ns; ++i) {
               if (n > 0) {
@@ -361,43 +422,43 @@ __device__ void run_support(const KParams& p, uint8_t* smem_raw, Shared* sh, uin
                 dev::mbar_wait(&sh->p_full[i], nblk[i] & 1);
                 ++nblk[i];
                 dev::tc_fence_after();
-                if (i == 0) dbg(p, 6, gb + n - 1);
+                dbg(p, i == 0 ? 6 : 13, gb + n - 1);
                 issue_pv(i, i, sV, n == 1);
               }
-              if (i == 0) dbg(p, 5, gb + n);
+              dbg(p, i == 0 ? 5 : 12, gb + n);
               issue_s(i, i, sK);
             }
-            if (n > 0) dev::mma_commit(&sh->ring_empty[sV]);
-            dev::mma_commit(&sh->ring_empty[sK]);
+            if (n > 0) PSA_MMA_COMMIT(&sh->ring_empty[sV]);
+            PSA_MMA_COMMIT(&sh->ring_empty[sK]);
           }
-          dev::mma_commit(&sh->q_empty);  // every S of this item issued
-          const uint32_t cV = 2 * (gb + nb) - 1, sV = cV % NR;
-          dev::mbar_wait(&sh->ring_full[sV], (cV / NR) & 1);
+          PSA_MMA_COMMIT(&sh->q_empty);  // every S of this item issued
+          const uint32_t sV = R.vslot(gb + nb - 1);
+          dev::mbar_wait(&sh->ring_full[sV], R.vpar(gb + nb - 1));
           for (int i = 0; i < ns; ++i) {
             if (nb == 1) dev::mbar_wait(&sh->o_empty[i], (nitem[i] & 1) ^ 1);
             dev::mbar_wait(&sh->p_full[i], nblk[i] & 1);
             ++nblk[i];
             dev::tc_fence_after();
             issue_pv(i, i, sV, nb == 1);
-            dev::mma_commit(&sh->o_full[i]);
+            PSA_MMA_COMMIT(&sh->o_full[i]);
             ++nitem[i];
           }
-          dev::mma_commit(&sh->ring_empty[sV]);
+          PSA_MMA_COMMIT(&sh->ring_empty[sV]);
         } else {
           // one slot: S ping-pongs between both S buffers (block n -> buffer n & 1), so
           // S(n + 1) is computed while the softmax works on block n. Order: S(0), S(1),
           // PV(0), S(2), PV(1), ...: S(n) overwrites P(n - 2) after PV(n - 2) was issued.
           for (int n = 0; n < nb; ++n) {
-            const uint32_t cK = 2 * (gb + n), sK = cK % NR;
-            dev::mbar_wait(&sh->ring_full[sK], (cK / NR) & 1);
+            const uint32_t jK = gb + n, sK = R.kslot(jK);
+            dev::mbar_wait(&sh->ring_full[sK], R.kpar(jK));
             dev::tc_fence_after();
             dbg(p, 5, gb + n);
             issue_s(0, n & 1, sK);
-            dev::mma_commit(&sh->ring_empty[sK]);
-            if (n == nb - 1) dev::mma_commit(&sh->q_empty);  // every S of this item issued
+            PSA_MMA_COMMIT(&sh->ring_empty[sK]);
+            if (n == nb - 1) PSA_MMA_COMMIT(&sh->q_empty);  // every S of this item issued
             if (n > 0) {
-              const uint32_t cV = cK - 1, sV = cV % NR;  // V_{n-1}
-              dev::mbar_wait(&sh->ring_full[sV], (cV / NR) & 1);
+              const uint32_t sV = R.vslot(jK - 1);  // V_{n-1}
+              dev::mbar_wait(&sh->ring_full[sV], R.vpar(jK - 1));
               if (n == 1) dev::mbar_wait(&sh->o_empty[0], (nitem[0] & 1) ^ 1);
               const int b = (n - 1) & 1;
               dev::mbar_wait(&sh->p_full[b], nblk[b] & 1);
@@ -405,22 +466,22 @@ __device__ void run_support(const KParams& p, uint8_t* smem_raw, Shared* sh, uin
               dev::tc_fence_after();
               dbg(p, 6, gb + n - 1);
               issue_pv(b, 0, sV, n == 1);
-              dev::mma_commit(&sh->pv_done);
-              dev::mma_commit(&sh->ring_empty[sV]);
+              PSA_MMA_COMMIT(&sh->pv_done);
+              PSA_MMA_COMMIT(&sh->ring_empty[sV]);
             }
           }
-          const uint32_t cV = 2 * (gb + nb) - 1, sV = cV % NR;  // V_{nb-1}
-          dev::mbar_wait(&sh->ring_full[sV], (cV / NR) & 1);
+          const uint32_t sV = R.vslot(gb + nb - 1);  // V_{nb-1}
+          dev::mbar_wait(&sh->ring_full[sV], R.vpar(gb + nb - 1));
           if (nb == 1) dev::mbar_wait(&sh->o_empty[0], (nitem[0] & 1) ^ 1);
           const int b = (nb - 1) & 1;
           dev::mbar_wait(&sh->p_full[b], nblk[b] & 1);
           ++nblk[b];
           dev::tc_fence_after();
           issue_pv(b, 0, sV, nb == 1);
-          dev::mma_commit(&sh->pv_done);
-          dev::mma_commit(&sh->o_full[0]);
+          PSA_MMA_COMMIT(&sh->pv_done);
+          PSA_MMA_COMMIT(&sh->o_full[0]);
           ++nitem[0];
-          dev::mma_commit(&sh->ring_empty[sV]);
+          PSA_MMA_COMMIT(&sh->ring_empty[sV]);
         }
         gb += nb;
       }
@@ -491,6 +552,7 @@ __device__ void run_softmax(const KParams& p, Shared* sh, uint32_t tmem, LoadIte
         const uint32_t tS = tmem + uint32_t(b) * 128 + lane_base;
         const bool ev = threadIdx.x == 0;
         if (ev) dbg(p, 0, nblk);
+        if (threadIdx.x == 128) dbg(p, 9, nblk);
         dev::tc_fence_after();
         uint32_t r[4][32];
         dev::tmem_ld32(tS + 0, r[0]);
@@ -511,6 +573,9 @@ __device__ void run_softmax(const KParams& p, Shared* sh, uint32_t tmem, LoadIte
             for (int e = 0; e < 32; ++e)
               if (c * 32 + e >= ncut) r[c][e] = 0xff800000u;
         }
+#ifdef PSA_EXP_SKIP  // timing diagnostics only (results wrong): no max / exp work
+        const float mraw = 0.f;
+#else
         // row max of the raw scores (scale > 0): 8 independent FMNMX3 chains
         float a8[8];
 #pragma unroll
@@ -522,6 +587,7 @@ __device__ void run_softmax(const KParams& p, Shared* sh, uint32_t tmem, LoadIte
           a8[j] = acc;
         }
         const float mraw = max3(max3(a8[0], a8[1], a8[2]), max3(a8[3], a8[4], a8[5]), fmaxf(a8[6], a8[7]));
+#endif
         const float mb = mraw * sc;
         if (ev) dbg(p, 2, nblk);
         float alpha = 1.f;
@@ -542,6 +608,11 @@ __device__ void run_softmax(const KParams& p, Shared* sh, uint32_t tmem, LoadIte
 #pragma unroll
           for (int e = 0; e < 16; ++e) {
             float x0, x1, y0, y1;
+#ifdef PSA_EXP_SKIP
+            y0 = __uint_as_float(r[c][2 * e]); y1 = __uint_as_float(r[c][2 * e + 1]);
+            r[c][e] = pack2<T>(y0, y1);
+            continue;
+#endif
             ffma2(x0, x1, __uint_as_float(r[c][2 * e]), __uint_as_float(r[c][2 * e + 1]), sc, nm);
             if (kEmuEvery > 0 && ((c * 16 + e) % kEmuEvery) == kEmuEvery - 1) {
               exp2_poly2(y0, y1, x0, x1);
@@ -554,6 +625,7 @@ __device__ void run_softmax(const KParams& p, Shared* sh, uint32_t tmem, LoadIte
           }
         }
         if (ev) dbg(p, 3, nblk);
+        if (threadIdx.x == 128) dbg(p, 10, nblk);
         // P_n -> S_i columns [0, 64)
         {
           uint32_t hi[32];
@@ -588,6 +660,7 @@ __device__ void run_softmax(const KParams& p, Shared* sh, uint32_t tmem, LoadIte
         __syncwarp();
         if (lane == 0) dev::mbar_arrive(&sh->p_full[b]);
         if (ev) dbg(p, 4, nblk);
+        if (threadIdx.x == 128) dbg(p, 11, nblk);
       }
       if (two) {
         if (i == 0) hs[1] += uint32_t(nb);  // WG1 consumed buffer 1's phases

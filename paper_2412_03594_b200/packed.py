@@ -299,7 +299,7 @@ class PrefixSharedAttention:
         finally:
             L.lib().psa_debug_set_trace(None, 0)
         out = buf.cpu().numpy()
-        self.last_tile_events = out[n:].reshape(-1)[:9 * 64].reshape(9, 64)
+        self.last_tile_events = out[n:].reshape(-1)[:14 * 64].reshape(14, 64)
         self.last_dec_events = out[n:].reshape(-1)[16 * 64:33 * 64].reshape(17, 64)
         self.last_merge_tasks = out[n:].reshape(-1)[36 * 64:40 * 64].reshape(4, 64)
         self.last_dec_events2 = out[n:].reshape(-1)[40 * 64:43 * 64].reshape(3, 64)

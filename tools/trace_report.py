@@ -94,7 +94,8 @@ def main():
     if ev is not None and op.plan_tables()["num_tile_items"] > 0 and ev[0, 0] != 0 and args.tile2:
         # v2 tile events (CTA 0, slot 0): clock64 per block
         names = ["s_ready", "ld_done", "max_done", "exp_done", "p_arrive", "s_issue", "pv_issue",
-                 "k_issue", "v_issue"]
+                 "k_issue", "v_issue", "s1_ready", "s1_exp_done", "s1_p_arrive", "s1_s_issue",
+                 "s1_pv_issue"]
         t0 = ev[7, 0]
         nb = int((ev[0] != 0).sum())
         rep["tile2_events_cycles"] = {nm: [int(x - t0) if x else 0 for x in ev[i, :min(nb, 24)]]
