@@ -369,7 +369,14 @@ __device__ void run(const KParams& p, uint8_t* smem_raw, Shared* sh, uint32_t tm
     }
   } else if (warp == 5) {
     // ================= MMA issuer =================
-    if (lane == 0) {
+    if (PSA_MMA_WARP_WIDE || lane == 0) {
+      // warp-wide issue (PSA_MMA_WARP_WIDE): every barrier test is lane 0's verdict,
+      // so the branches stay warp-uniform around the elect.sync issue forms
+      auto test = [&](uint64_t* bar, uint32_t par) {
+        bool r = dev::mbar_test(bar, par);
+        if (PSA_MMA_WARP_WIDE) r = __shfl_sync(0xffffffffu, int(r), 0) != 0;
+        return r;
+      };
       constexpr uint32_t fmt = tile::AbFormat<T>::v;
       const uint32_t idesc_s = dev::umma_idesc_f16(fmt, kBK, kN, 0, 0);
       const uint32_t idesc_o = dev::umma_idesc_f16(fmt, 128, kN, 1, 0);
@@ -387,7 +394,7 @@ __device__ void run(const KParams& p, uint8_t* smem_raw, Shared* sh, uint32_t tm
         // ---- S stream
         if (!s_done) {
           const uint32_t q = k_s & 1;
-          if (nb_s < 0 && dev::mbar_test(&sh->item_full[q], (k_s >> 1) & 1)) {
+          if (nb_s < 0 && test(&sh->item_full[q], (k_s >> 1) & 1)) {
             const int idx = sh->item_idx[q];
             if (idx < 0) {
               s_done = true;
@@ -403,28 +410,30 @@ __device__ void run(const KParams& p, uint8_t* smem_raw, Shared* sh, uint32_t tm
           }
           if (nb_s > 0) {
             const uint32_t cK = 2 * gS, s = cK % NSL;
-            const bool sfree = gS == 0 || dev::mbar_test(&sh->s_free, (gS - 1) & 1);
+            const bool sfree = gS == 0 || test(&sh->s_free, (gS - 1) & 1);
             // A parity test tells phase o from phase o - 2 only once phase o - 1 has
             // completed. With an odd ring, K_g's slot previously held V_j (cK - NSL =
             // 2j + 1), which only the PV stream waits for: require PV_j issued (so V_j
             // landed), else K_g's test could pass on phase o - 2 while V_j is in flight.
             const int32_t prev = int32_t(cK) - int32_t(NSL);
             const bool prev_ok = prev < 0 || !(prev & 1) || gP > uint32_t((prev - 1) >> 1);
-            if (sfree && prev_ok && dev::mbar_test(&sh->slot_full[s], (cK / NSL) & 1)) {
+            if (sfree && prev_ok && test(&sh->slot_full[s], (cK / NSL) & 1)) {
               dev::tc_fence_after();
               dbg(p, 2, gS);
-              const uint32_t a0 = dev::smem_u32(G.slot(s)), b0 = dev::smem_u32(G.q(q));
-              for (int kk = 0; kk < 8; ++kk) {
+              const uint64_t ad = dev::umma_desc_sw128(dev::smem_u32(G.slot(s)), 16, 1024);
+              const uint64_t bd0 = dev::umma_desc_sw128(dev::smem_u32(G.q(q)), 16, 1024);
+#pragma unroll
+              for (int kk = 0; kk < 8; ++kk) {  // descriptor start address is addr >> 4
                 const uint32_t ch = kk >> 2, w = (kk & 3) * 32;
-                const uint64_t a = dev::umma_desc_sw128(a0 + ch * (kBK * 128) + w, 16, 1024);
-                const uint64_t b = dev::umma_desc_sw128(b0 + ch * (kN * 128) + w, 16, 1024);
-                dev::mma_f16_ss(tS, a, b, idesc_s, kk > 0);
+                const uint64_t a = ad + uint64_t((ch * (kBK * 128) + w) >> 4);
+                const uint64_t b = bd0 + uint64_t((ch * (kN * 128) + w) >> 4);
+                PSA_MMA_SS(tS, a, b, idesc_s, kk > 0);
               }
-              dev::mma_commit(&sh->s_full);
-              dev::mma_commit(&sh->slot_empty[s]);
+              PSA_MMA_COMMIT(&sh->s_full);
+              PSA_MMA_COMMIT(&sh->slot_empty[s]);
               ++gS;
               if (++j_s == nb_s) {
-                dev::mma_commit(&sh->item_empty[q]);  // Q slot reusable once these S complete
+                PSA_MMA_COMMIT(&sh->item_empty[q]);  // Q slot reusable once these S complete
                 nb_s = -1;
                 ++k_s;
               }
@@ -438,23 +447,25 @@ __device__ void run(const KParams& p, uint8_t* smem_raw, Shared* sh, uint32_t tm
           if (nb_p < 0) { nb_p = nbs_ring[q]; j_p = 0; }
           const uint32_t cV = 2 * gP + 1, s = cV % NSL;
           const bool need_o = j_p == 0;
-          if (dev::mbar_test(&sh->p_full[gP & 1], (gP >> 1) & 1) &&
-              dev::mbar_test(&sh->slot_full[s], (cV / NSL) & 1) &&
-              (!need_o || dev::mbar_test(&sh->o_empty[b], ((k_p >> 1) & 1) ^ 1))) {
+          if (test(&sh->p_full[gP & 1], (gP >> 1) & 1) &&
+              test(&sh->slot_full[s], (cV / NSL) & 1) &&
+              (!need_o || test(&sh->o_empty[b], ((k_p >> 1) & 1) ^ 1))) {
             dev::tc_fence_after();
             dbg(p, 3, gP);
-            const uint32_t a0 = dev::smem_u32(G.slot(s));
+            const uint64_t ad = dev::umma_desc_sw128(dev::smem_u32(G.slot(s)), kBK * 128, 1024);
+            const uint64_t pd = dev::umma_desc_sw128(pt, 16, 1024);
             const uint32_t tO = tmem + kTmemO + b * kN;
+#pragma unroll
             for (int kk = 0; kk < kBK / 16; ++kk) {
-              const uint64_t a = dev::umma_desc_sw128(a0 + kk * (16 * 128), kBK * 128, 1024);
-              const uint64_t bd = dev::umma_desc_sw128(pt + (kk >> 2) * (kN * 128) + (kk & 3) * 32, 16, 1024);
-              dev::mma_f16_ss(tO, a, bd, idesc_o, (j_p > 0 || kk > 0));
+              const uint64_t a = ad + uint64_t((kk * (16 * 128)) >> 4);
+              const uint64_t bd = pd + uint64_t(((kk >> 2) * (kN * 128) + (kk & 3) * 32) >> 4);
+              PSA_MMA_SS(tO, a, bd, idesc_o, (j_p > 0 || kk > 0));
             }
-            dev::mma_commit(&sh->slot_empty[s]);
-            dev::mma_commit(&sh->o_done);
+            PSA_MMA_COMMIT(&sh->slot_empty[s]);
+            PSA_MMA_COMMIT(&sh->o_done);
             ++gP;
             if (++j_p == nb_p) {
-              dev::mma_commit(&sh->o_full[b]);
+              PSA_MMA_COMMIT(&sh->o_full[b]);
               nb_p = -1;
               ++k_p;
             }

@@ -238,6 +238,25 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&r)[32]) {
       : PSA_R32(r)
       : "r"(taddr));
 }
+
+// PSA_MMA_WARP_WIDE (default): the MMA role runs on all 32 lanes of its warp and
+// issues through elect.sync (psa_device.cuh *_w forms), so ptxas emits straight-line
+// UTCHMMA sequences instead of one elect/R2UR waterfall loop per instruction (the
+// lane-0 form spent ~85 cycles issuing each 64-cycle MMA: c3 2985 -> 2801 us, c4
+// 612 -> 600 us, c5 15.5 -> 14.6 ms). 0 = lane 0 alone (diagnostics).
+#ifndef PSA_MMA_WARP_WIDE
+#define PSA_MMA_WARP_WIDE 1
+#endif
+#if PSA_MMA_WARP_WIDE
+#define PSA_MMA_TS ::psa::dev::mma_f16_ts_w
+#define PSA_MMA_SS ::psa::dev::mma_f16_ss_w
+#define PSA_MMA_COMMIT ::psa::dev::mma_commit_w
+#else
+#define PSA_MMA_TS ::psa::dev::mma_f16_ts
+#define PSA_MMA_SS ::psa::dev::mma_f16_ss
+#define PSA_MMA_COMMIT ::psa::dev::mma_commit
+#endif
+
 __device__ __forceinline__ void tmem_st32(uint32_t taddr, const uint32_t (&r)[32]) {
   asm volatile(
       "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8, %9, %10, "
