@@ -1028,7 +1028,10 @@ __global__ void __launch_bounds__(kThreads, 2) psa_persistent(const __grid_const
 // queue; the last CTA out resets both cursors.
 // ---------------------------------------------------------------------------
 constexpr int kV2Threads = 512;
-constexpr int kV2EmuEvery = 4;  // every 4th exp pair of the tile softmax on the FMA pipe
+#ifndef PSA_EMU_EVERY
+#define PSA_EMU_EVERY 4
+#endif
+constexpr int kV2EmuEvery = PSA_EMU_EVERY;  // every 4th exp pair of the tile softmax on the FMA pipe
 
 __device__ __forceinline__ void setmaxnreg_inc_168() { asm volatile("setmaxnreg.inc.sync.aligned.u32 168;"); }
 __device__ __forceinline__ void setmaxnreg_dec_88() { asm volatile("setmaxnreg.dec.sync.aligned.u32 88;"); }
