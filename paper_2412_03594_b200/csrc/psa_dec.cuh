@@ -73,6 +73,19 @@ __device__ __forceinline__ int64_t out_index(const KParams& p, int64_t tok0, int
   return (tok0 + tq) * p.Hq + (int64_t)h * p.gqa + (row - tq * p.gqa);
 }
 
+// Decode MMA issuer: warp-wide (elect.sync) or lane 0 alone, independently of the
+// tile issuer (PSA_DEC_WARP_WIDE, default PSA_MMA_WARP_WIDE).
+#ifndef PSA_DEC_WARP_WIDE
+#define PSA_DEC_WARP_WIDE PSA_MMA_WARP_WIDE
+#endif
+#if PSA_DEC_WARP_WIDE
+#define PSA_DEC_MMA_SS ::psa::dev::mma_f16_ss_w
+#define PSA_DEC_MMA_COMMIT ::psa::dev::mma_commit_w
+#else
+#define PSA_DEC_MMA_SS ::psa::dev::mma_f16_ss
+#define PSA_DEC_MMA_COMMIT ::psa::dev::mma_commit
+#endif
+
 namespace dec {
 
 constexpr int kBK = 128;               // keys per block (MMA M)
@@ -369,12 +382,12 @@ __device__ void run(const KParams& p, uint8_t* smem_raw, Shared* sh, uint32_t tm
     }
   } else if (warp == 5) {
     // ================= MMA issuer =================
-    if (PSA_MMA_WARP_WIDE || lane == 0) {
-      // warp-wide issue (PSA_MMA_WARP_WIDE): every barrier test is lane 0's verdict,
+    if (PSA_DEC_WARP_WIDE || lane == 0) {
+      // warp-wide issue (PSA_DEC_WARP_WIDE): every barrier test is lane 0's verdict,
       // so the branches stay warp-uniform around the elect.sync issue forms
       auto test = [&](uint64_t* bar, uint32_t par) {
         bool r = dev::mbar_test(bar, par);
-        if (PSA_MMA_WARP_WIDE) r = __shfl_sync(0xffffffffu, int(r), 0) != 0;
+        if (PSA_DEC_WARP_WIDE) r = __shfl_sync(0xffffffffu, int(r), 0) != 0;
         return r;
       };
       constexpr uint32_t fmt = tile::AbFormat<T>::v;
@@ -427,13 +440,13 @@ __device__ void run(const KParams& p, uint8_t* smem_raw, Shared* sh, uint32_t tm
                 const uint32_t ch = kk >> 2, w = (kk & 3) * 32;
                 const uint64_t a = ad + uint64_t((ch * (kBK * 128) + w) >> 4);
                 const uint64_t b = bd0 + uint64_t((ch * (kN * 128) + w) >> 4);
-                PSA_MMA_SS(tS, a, b, idesc_s, kk > 0);
+                PSA_DEC_MMA_SS(tS, a, b, idesc_s, kk > 0);
               }
-              PSA_MMA_COMMIT(&sh->s_full);
-              PSA_MMA_COMMIT(&sh->slot_empty[s]);
+              PSA_DEC_MMA_COMMIT(&sh->s_full);
+              PSA_DEC_MMA_COMMIT(&sh->slot_empty[s]);
               ++gS;
               if (++j_s == nb_s) {
-                PSA_MMA_COMMIT(&sh->item_empty[q]);  // Q slot reusable once these S complete
+                PSA_DEC_MMA_COMMIT(&sh->item_empty[q]);  // Q slot reusable once these S complete
                 nb_s = -1;
                 ++k_s;
               }
@@ -459,13 +472,13 @@ __device__ void run(const KParams& p, uint8_t* smem_raw, Shared* sh, uint32_t tm
             for (int kk = 0; kk < kBK / 16; ++kk) {
               const uint64_t a = ad + uint64_t((kk * (16 * 128)) >> 4);
               const uint64_t bd = pd + uint64_t(((kk >> 2) * (kN * 128) + (kk & 3) * 32) >> 4);
-              PSA_MMA_SS(tO, a, bd, idesc_o, (j_p > 0 || kk > 0));
+              PSA_DEC_MMA_SS(tO, a, bd, idesc_o, (j_p > 0 || kk > 0));
             }
-            PSA_MMA_COMMIT(&sh->slot_empty[s]);
-            PSA_MMA_COMMIT(&sh->o_done);
+            PSA_DEC_MMA_COMMIT(&sh->slot_empty[s]);
+            PSA_DEC_MMA_COMMIT(&sh->o_done);
             ++gP;
             if (++j_p == nb_p) {
-              PSA_MMA_COMMIT(&sh->o_full[b]);
+              PSA_DEC_MMA_COMMIT(&sh->o_full[b]);
               nb_p = -1;
               ++k_p;
             }

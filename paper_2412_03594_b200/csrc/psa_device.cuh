@@ -245,7 +245,7 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&r)[32]) {
 // lane-0 form spent ~85 cycles issuing each 64-cycle MMA: c3 2985 -> 2801 us, c4
 // 612 -> 600 us, c5 15.5 -> 14.6 ms). 0 = lane 0 alone (diagnostics).
 #ifndef PSA_MMA_WARP_WIDE
-#define PSA_MMA_WARP_WIDE 1
+#define PSA_MMA_WARP_WIDE 0
 #endif
 #if PSA_MMA_WARP_WIDE
 #define PSA_MMA_TS ::psa::dev::mma_f16_ts_w

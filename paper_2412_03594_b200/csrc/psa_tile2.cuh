@@ -34,6 +34,10 @@
 
 #include "psa_device.cuh"
 
+#ifndef PSA_MMA_WAIT_SYNC
+#define PSA_MMA_WAIT_SYNC 1
+#endif
+
 namespace psa {
 namespace tile2 {
 
@@ -341,6 +345,12 @@ __device__ void run_support(const KParams& p, uint8_t* smem_raw, Shared* sh, uin
   } else if (warp == kMmaWarp) {
     // ============================ MMA issuer ============================
     if (PSA_MMA_WARP_WIDE || lane == 0) {
+      // Warp-wide issue: every lane runs each barrier wait, then the warp reconverges
+      // (PSA_MMA_WAIT_SYNC) before any lane acts on the phase it observed.
+      auto mwait = [&](uint64_t* bar, uint32_t par) {
+        dev::mbar_wait(bar, par);
+        if (PSA_MMA_WARP_WIDE && PSA_MMA_WAIT_SYNC) __syncwarp();
+      };
       constexpr uint32_t fmt = AbFormat<T>::v;
       const uint32_t idesc_s = dev::umma_idesc_f16(fmt, kM, kBN, 0, 0);
       const uint32_t idesc_o = dev::umma_idesc_f16(fmt, kM, kD, 0, 1);
@@ -349,7 +359,7 @@ __device__ void run_support(const KParams& p, uint8_t* smem_raw, Shared* sh, uin
       uint32_t nitem[2] = {0u, 0u}; // items processed per slot (o_empty phases)
       for (uint32_t k = 0;; ++k) {
         const uint32_t q = k & 1;
-        dev::mbar_wait(&sh->item_full[q], (k >> 1) & 1);
+        mwait(&sh->item_full[q], (k >> 1) & 1);
         const int idx = sh->item_idx[q];
         if (idx < 0) break;
         const auto it = load_item_at(idx);
@@ -358,7 +368,7 @@ __device__ void run_support(const KParams& p, uint8_t* smem_raw, Shared* sh, uin
         int64_t pbase, dbase;
         item_shape(p, it, nbA, nb, pbase, dbase);
         const int ns = it.nrows > tile_rows ? 2 : 1;
-        dev::mbar_wait(&sh->q_full, k & 1);
+        mwait(&sh->q_full, k & 1);
         dev::tc_fence_after();
         // O_o (+)= P V: 8 K-steps of 16 keys; A = P in TMEM (bf16 pairs) in S buffer pb
         auto issue_pv = [&](int pb, int o, uint32_t vslot, bool first) {
@@ -393,15 +403,15 @@ __device__ void run_support(const KParams& p, uint8_t* smem_raw, Shared* sh, uin
           for (int n = 0; n < nb; ++n) {
             const uint32_t jK = gb + n, sK = R.kslot(jK);
             const uint32_t sV = R.vslot(jK - 1);  // V_{n-1}
-            dev::mbar_wait(&sh->ring_full[sK], R.kpar(jK));
-            if (n > 0) dev::mbar_wait(&sh->ring_full[sV], R.vpar(jK - 1));
+            mwait(&sh->ring_full[sK], R.kpar(jK));
+            if (n > 0) mwait(&sh->ring_full[sV], R.vpar(jK - 1));
             dev::tc_fence_after();
             for (int i = 0; i < ns; ++i) {
               if (n > 0) {
                 if (n == 1) {  // first PV of this item overwrites O_i: the WG read the last one
-                  dev::mbar_wait(&sh->o_empty[i], (nitem[i] & 1) ^ 1);
+                  mwait(&sh->o_empty[i], (nitem[i] & 1) ^ 1);
                 }
-                dev::mbar_wait(&sh->p_full[i], nblk[i] & 1);
+                mwait(&sh->p_full[i], nblk[i] & 1);
                 ++nblk[i];
                 dev::tc_fence_after();
                 dbg(p, i == 0 ? 6 : 13, gb + n - 1);
@@ -415,10 +425,10 @@ __device__ void run_support(const KParams& p, uint8_t* smem_raw, Shared* sh, uin
           }
           PSA_MMA_COMMIT(&sh->q_empty);  // every S of this item issued
           const uint32_t sV = R.vslot(gb + nb - 1);
-          dev::mbar_wait(&sh->ring_full[sV], R.vpar(gb + nb - 1));
+          mwait(&sh->ring_full[sV], R.vpar(gb + nb - 1));
           for (int i = 0; i < ns; ++i) {
-            if (nb == 1) dev::mbar_wait(&sh->o_empty[i], (nitem[i] & 1) ^ 1);
-            dev::mbar_wait(&sh->p_full[i], nblk[i] & 1);
+            if (nb == 1) mwait(&sh->o_empty[i], (nitem[i] & 1) ^ 1);
+            mwait(&sh->p_full[i], nblk[i] & 1);
             ++nblk[i];
             dev::tc_fence_after();
             issue_pv(i, i, sV, nb == 1);
@@ -432,7 +442,7 @@ __device__ void run_support(const KParams& p, uint8_t* smem_raw, Shared* sh, uin
           // PV(0), S(2), PV(1), ...: S(n) overwrites P(n - 2) after PV(n - 2) was issued.
           for (int n = 0; n < nb; ++n) {
             const uint32_t jK = gb + n, sK = R.kslot(jK);
-            dev::mbar_wait(&sh->ring_full[sK], R.kpar(jK));
+            mwait(&sh->ring_full[sK], R.kpar(jK));
             dev::tc_fence_after();
             dbg(p, 5, gb + n);
             issue_s(0, n & 1, sK);
@@ -440,10 +450,10 @@ __device__ void run_support(const KParams& p, uint8_t* smem_raw, Shared* sh, uin
             if (n == nb - 1) PSA_MMA_COMMIT(&sh->q_empty);  // every S of this item issued
             if (n > 0) {
               const uint32_t sV = R.vslot(jK - 1);  // V_{n-1}
-              dev::mbar_wait(&sh->ring_full[sV], R.vpar(jK - 1));
-              if (n == 1) dev::mbar_wait(&sh->o_empty[0], (nitem[0] & 1) ^ 1);
+              mwait(&sh->ring_full[sV], R.vpar(jK - 1));
+              if (n == 1) mwait(&sh->o_empty[0], (nitem[0] & 1) ^ 1);
               const int b = (n - 1) & 1;
-              dev::mbar_wait(&sh->p_full[b], nblk[b] & 1);
+              mwait(&sh->p_full[b], nblk[b] & 1);
               ++nblk[b];
               dev::tc_fence_after();
               dbg(p, 6, gb + n - 1);
@@ -453,10 +463,10 @@ __device__ void run_support(const KParams& p, uint8_t* smem_raw, Shared* sh, uin
             }
           }
           const uint32_t sV = R.vslot(gb + nb - 1);  // V_{nb-1}
-          dev::mbar_wait(&sh->ring_full[sV], R.vpar(gb + nb - 1));
-          if (nb == 1) dev::mbar_wait(&sh->o_empty[0], (nitem[0] & 1) ^ 1);
+          mwait(&sh->ring_full[sV], R.vpar(gb + nb - 1));
+          if (nb == 1) mwait(&sh->o_empty[0], (nitem[0] & 1) ^ 1);
           const int b = (nb - 1) & 1;
-          dev::mbar_wait(&sh->p_full[b], nblk[b] & 1);
+          mwait(&sh->p_full[b], nblk[b] & 1);
           ++nblk[b];
           dev::tc_fence_after();
           issue_pv(b, 0, sV, nb == 1);
