@@ -351,6 +351,9 @@ psa_status psa_run(const psa_problem* prob, const psa_plan* pl, void* ws, size_t
   k.Hq = in.Hq; k.Hkv = in.Hkv; k.gqa = in.Hq / in.Hkv; k.d = in.d; k.dv = in.dv;
   k.max_vec_rows = pl->plan.max_vec_rows;
   k.dec_help = pl->plan.vec_fan_in > 2 ? 1 : 0;  // two: the in-register pair merge covers it
+#ifdef PSA_NO_DEC_HELP
+  k.dec_help = 0;  // diagnostics build: decode merge queues drained by their merge warps only
+#endif
   k.gqa_shift = -1;
   for (int sh = 0; sh < 31; ++sh)
     if ((1 << sh) == k.gqa) k.gqa_shift = sh;
